@@ -1,0 +1,348 @@
+"""Benchmark: AMG setup + solve time to relative residual 1e-8 on the 3D
+7-point Poisson problem (BASELINE.json config C2, 128^3 = 2,097,152 unknowns)
+plus the level-0 SpMV / smoother HBM bandwidth.
+
+One step = build the full hierarchy from the device-resident CSR (setup) and
+run K-cycle / l1-Jacobi NPCG from x0 = 0 with b = 1 to relres 1e-8 (solve),
+exactly the reference's ``setup(A)`` + ``npcg_solve(h, CycleSpec(),
+Smoother(), b, tol=1e-8)``.  value = seconds per step (max over ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): every rank solves its own copy of the
+problem (weak scaling, replicas -- the row-block partition is not built yet,
+see DESIGN.md); timing is the max over ranks of device time.
+``--impl reference`` times the CPU oracle port of the reference path
+(oracle/, C + OpenMP, all host cores) on the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "AMG setup+solve sec to relres 1e-8 (3D Poisson); SpMV/smoother HBM GB/s"
+WORKLOAD = "C2: 3D 7-point Laplacian 128^3 (2,097,152 unknowns), device setup + K-cycle/l1-Jacobi NPCG to 1e-8"
+TOL = 1e-8
+N_GRID = 128
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, ws, local
+
+
+def peak_hbm():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if len(s) > 5 + k and s[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def build_problem():
+    from paper_1302_2547_b200 import problems
+    return problems.grid3d(N_GRID, 7)
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, ws):
+    """CPU oracle port (oracle/uaamg_oracle.c, OpenMP on every host core)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    O.set_num_threads(cores)
+    A = build_problem()
+    b = np.ones(A.n_rows)
+
+    def step():
+        t0 = time.perf_counter()
+        h = O.setup(A.indptr, A.indices, A.data)
+        _, rep = O.npcg_solve(h, b, tol=TOL, max_iters=500)
+        return time.perf_counter() - t0, rep.iterations
+
+    for _ in range(min(args.warmup, 1)):
+        step()
+    times, its = [], 0
+    for _ in range(args.steps):
+        t, its = step()
+        times.append(t)
+    v = sum(times) / len(times)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1)",
+            "config": {"workload": WORKLOAD, "iterations": its, "tol": TOL},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
+                             "sample": "full C2 setup + NPCG solve to 1e-8 per step (CPU oracle, C/OpenMP)"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(A):
+    """Bounded CPU sample for our arm's line: one full C2 setup + solve."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    O.set_num_threads(cores)
+    b = np.ones(A.n_rows)
+    t0 = time.perf_counter()
+    h = O.setup(A.indptr, A.indices, A.data)
+    t1 = time.perf_counter()
+    _, rep = O.npcg_solve(h, b, tol=TOL, max_iters=500)
+    t2 = time.perf_counter()
+    return {"value": t2 - t0, "unit": "s", "cores": cores, "kind": "port",
+            "sample": f"one full C2 setup ({t1 - t0:.2f} s) + solve ({t2 - t1:.2f} s, {rep.iterations} it), "
+                      "CPU oracle C/OpenMP"}
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, rank, ws, local):
+    import torch
+    import paper_1302_2547_b200 as U
+    from paper_1302_2547_b200 import _lib
+    from paper_1302_2547_b200.device import DeviceCSR
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    A = build_problem()
+    n = A.n_rows
+    # inputs resident in HBM for `value`
+    Ad = DeviceCSR.from_host(A)
+    b = torch.ones(n, dtype=torch.float64, device=dev)
+    spec, sm = U.CycleSpec(), U.Smoother()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(profile=False):
+        h = U.setup(Ad)
+        x, rep = solve(h, profile)
+        return h, x, rep
+
+    def solve(h, profile):
+        import ctypes
+        from paper_1302_2547_b200.solvers import _params
+        P = _params(spec, sm, TOL, 500, True)
+        P.profile_level0 = int(profile)
+        res = _lib.SolveResult()
+        x = torch.empty(n, dtype=torch.float64, device=dev)
+        hist = np.zeros(501)
+        _lib.check(_lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), b.data_ptr(), None, x.data_ptr(),
+                                                hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
+                                                stream.cuda_stream))
+        return x, (res.iterations, hist[: res.iterations + 1])
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        step()
+    # timed region: per-step CUDA events, L2 flushed between steps (outside the events)
+    launches0 = _lib.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters = None
+    setup_s, solve_s = [], []
+    prof = {"secs": np.zeros(3), "bytes": None, "count": 0}
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            h, x, (iters, hist) = step(profile=True)
+            evs[k][1].record(stream)
+            setup_s.append(h.setup_seconds)
+            secs = np.zeros(3)
+            byts = np.zeros(3)
+            cnt = np.zeros(1, dtype=np.int64)
+            _lib.check(_lib.load().uaamg_solve_profile(h._handle, secs.ctypes.data, byts.ctypes.data,
+                                                       cnt.ctypes.data))
+            prof["secs"] += secs
+            prof["count"] += int(cnt[0])
+            prof["bytes"] = byts
+            del h
+        barrier()
+    launches = _lib.launch_count() - launches0
+    ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(args.steps)]
+    t_step = sum(ms) / len(ms) / 1e3
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    # correctness of the timed result (true residual of the last step)
+    r = (A.spmv(x.cpu().numpy()) - 1.0)
+    relres = float(np.linalg.norm(r) / np.sqrt(n))
+
+    # ---- e2e through the public API with host buffers (pinned), per step:
+    # H2D of the matrix + b, device setup + solve, D2H of x and the history
+    rp_h = torch.from_numpy(A.indptr.astype(np.int32)).pin_memory()
+    ci_h = torch.from_numpy(A.indices.astype(np.int32)).pin_memory()
+    av_h = torch.from_numpy(A.data).pin_memory()
+    b_h = torch.ones(n, dtype=torch.float64).pin_memory()
+    x_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    h2d = rp_h.numel() * 4 + ci_h.numel() * 4 + av_h.numel() * 8 + n * 8
+    d2h = n * 8
+
+    def e2e_step():
+        Ad2 = DeviceCSR(n, n, rp_h.to(dev, non_blocking=True), ci_h.to(dev, non_blocking=True),
+                        av_h.to(dev, non_blocking=True))
+        h2 = U.setup(Ad2)
+        xd, rep2 = U.npcg_solve(h2, spec, sm, b_h.to(dev, non_blocking=True), tol=TOL, max_iters=500)
+        x_h.copy_(xd, non_blocking=True)
+        torch.cuda.synchronize()
+        return rep2
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        rep2 = e2e_step()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    d2h += (rep2.iterations + 1) * 8
+
+    if rank != 0:
+        return
+    peak, peak_kind = peak_hbm()
+    names = ["residual", "up_sweep", "direction_spmv"]
+    kern = {}
+    for i, nm in enumerate(names):
+        if prof["count"] and prof["secs"][i] > 0:
+            per = prof["secs"][i] / prof["count"]
+            gbs = prof["bytes"][i] / per / 1e9
+            kern[nm] = {"us_per_launch": per * 1e6, "GBps": gbs, "frac": gbs / peak,
+                        "bytes_per_launch": float(prof["bytes"][i])}
+    dom = kern.get("up_sweep", {})
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "roofline_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("up_sweep_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cpu = cpu_baseline_sample(A) if ws == 1 else None
+    line = {
+        "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1, x0 = 0)",
+        "config": {"workload": WORKLOAD, "n": n, "nnz": A.nnz, "iterations": int(iters), "tol": TOL,
+                   "levels": None, "setup_s": float(np.mean(setup_s)),
+                   "solve_s": t_step - float(np.mean(setup_s)),
+                   "l2": "flushed between steps (256 MB write, outside the step events); matrix 175 MB > L2",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "true_relres": relres, "level0_kernels": kern},
+        "roofline": {"bound": "hbm", "kernel": "level-0 fused prolongation + l1-Jacobi post-sweep",
+                     "achieved": dom.get("GBps"), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": dom.get("frac"), "traffic": traffic},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "host pinned CSR + b -> DeviceCSR -> setup() -> npcg_solve() -> x to host"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    rank, ws, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, rank, ws)
+    else:
+        run_ours(args, rank, ws, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * uaamg_b200.h -- C ABI of the B200-native UA-AMG setup/solve path.
+ *
+ * Drop-in boundary for the reference package /root/reference/pkg/src/uaamg
+ * ("U/" below, "K/" = U/kernels/).  Two layers:
+ *
+ *   1. The kernel table.  The reference selects its hot kernels through a
+ *      16-name module table (K/__init__.py:37-54, plugin loader :14-34).  Each
+ *      uaamg_k_* entry below replaces one table entry, operating on DEVICE
+ *      pointers (int32 indices, float64 values) on the caller's CUDA stream.
+ *      Variable-size outputs are two-phase (count, then fill into caller
+ *      buffers).  INTEGRATION.md shows the ctypes backend module a maintainer
+ *      adds next to K/numba_backend.py to bind these.
+ *
+ *   2. The drivers.  uaamg_setup replaces U/hierarchy.py:120 setup() and
+ *      uaamg_npcg_solve replaces U/solvers.py:190 npcg_solve(); uaamg_cycle
+ *      replaces U/solvers.py:128 cycle().  The hierarchy stays device
+ *      resident behind an opaque handle.
+ *
+ * Conventions: every function returns 0 on success or a negative UAAMG_E*
+ * code; uaamg_last_error() returns a thread-local message for the last
+ * failure.  No C++ exceptions cross the ABI.  `stream` is a cudaStream_t (0 =
+ * legacy default stream).  All kernels are deterministic: results do not
+ * depend on grid size, stream, or timing (no floating-point atomics).
+ * Floating-point sums that the reference performs sequentially (row sums,
+ * aggregate sums, Galerkin entry sums) are performed in the same order
+ * without FMA contraction, so they are bit-identical to K/numba_backend.py.
+ */
+#ifndef UAAMG_B200_H
+#define UAAMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UAAMG_OK 0
+#define UAAMG_EINVAL (-1)      /* bad argument (reference: ValueError)            */
+#define UAAMG_ECUDA (-2)       /* CUDA runtime failure                             */
+#define UAAMG_ENUMERICAL (-3)  /* reference NumericalError (U/solvers.py:16-21)    */
+#define UAAMG_ESETUP (-4)      /* reference SetupError (U/hierarchy.py:18)         */
+#define UAAMG_EAGG (-5)        /* reference AggregationError (U/aggregation.py:21) */
+#define UAAMG_ENOMEM (-6)
+#define UAAMG_EUNSUPPORTED (-7)
+
+typedef struct uaamg_hierarchy uaamg_hierarchy;
+
+/* ------------------------------------------------------------------ */
+/* library                                                              */
+/* ------------------------------------------------------------------ */
+int uaamg_version(void);
+const char *uaamg_last_error(void);
+/* number of kernel launches issued by this library since load (all threads) */
+uint64_t uaamg_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* kernel table (replaces K/__init__.py:39-54 entries)                  */
+/* ------------------------------------------------------------------ */
+/* K/numba_backend.py:38-44  hash_u01(seed, pass_idx, idx) */
+int uaamg_k_hash_u01(uint64_t seed, int64_t pass_idx, const int64_t *idx, int64_t m, double *out, void *stream);
+/* K/numba_backend.py:47-56  spmv(indptr, indices, data, x) */
+int uaamg_k_spmv(int n, const int *row_ptr, const int *col, const double *val, const double *x, double *y,
+                 void *stream);
+/* K/numba_backend.py:59-68  diag_of */
+int uaamg_k_diag_of(int n, const int *row_ptr, const int *col, const double *val, double *out, void *stream);
+/* K/numba_backend.py:71-84  l1_diag */
+int uaamg_k_l1_diag(int n, const int *row_ptr, const int *col, const double *val, double *out, void *stream);
+/* K/numba_backend.py:87-97  degrees (int32 output) */
+int uaamg_k_degrees(int n, const int *row_ptr, const int *col, int *out, void *stream);
+/* K/numba_backend.py:100-111  quasi_random_scores */
+int uaamg_k_quasi_random_scores(int n, const int *row_ptr, const int *col, uint64_t seed, int64_t pass_idx,
+                                double *out, void *stream);
+/* K/numba_backend.py:114-142  squared_pattern: phase 1 counts (out_ptr[n+1]
+ * filled, *nnz2 returned), phase 2 (out_idx != NULL) fills sorted rows. */
+int uaamg_k_squared_pattern(int n, const int *row_ptr, const int *col, int *out_ptr, int *out_idx, int64_t *nnz2,
+                            void *stream);
+/* K/numba_backend.py:175-193  select_centers over an explicit pattern P
+ * (P = A^2 reproduces the reference exactly; the B200 setup path instead runs
+ * the same selection as two max-hops over A, see uaamg_k_select_centers_2hop). */
+int uaamg_k_select_centers(int n, const int *p_ptr, const int *p_idx, const double *scores,
+                           const uint8_t *processed, uint8_t *is_center, void *stream);
+/* same result as uaamg_k_select_centers(A^2 pattern) without forming A^2 */
+int uaamg_k_select_centers_2hop(int n, const int *row_ptr, const int *col, const double *scores,
+                                const uint8_t *processed, uint8_t *is_center, void *stream);
+/* K/numba_backend.py:196-220  claim_owners over an explicit pattern / 2-hop over A */
+int uaamg_k_claim_owners(int n, const int *p_ptr, const int *p_idx, const double *scores, const uint8_t *processed,
+                         const uint8_t *is_center, int *owner, void *stream);
+int uaamg_k_claim_owners_2hop(int n, const int *row_ptr, const int *col, const double *scores,
+                              const uint8_t *processed, const uint8_t *is_center, int *owner, void *stream);
+/* K/numba_backend.py:223-273  admit_members (in place on processed and
+ * vertex_to_agg; centers are listed with their buckets exactly as the
+ * reference's host glue builds them, U/aggregation.py:152-168).  cap<=0 means
+ * unlimited. */
+int uaamg_k_admit_members(int n, const int *row_ptr, const int *col, const double *val, int n_centers,
+                          const int *centers, const int *bucket_ptr, const int *bucket_js, int64_t cap,
+                          uint8_t *processed, int *vertex_to_agg, int agg_base, void *stream);
+/* K/numba_backend.py:145-172  galerkin_coo: phase 1 (out_col == NULL) fills
+ * out_ptr[nc+1] and *nnz_c; phase 2 fills out_col/out_val. */
+int uaamg_k_galerkin(int n, const int *row_ptr, const int *col, const double *val, const int *v2a, int nc,
+                     int *out_ptr, int *out_col, double *out_val, int64_t *nnz_c, void *stream);
+/* K/numba_backend.py:276-285  restrict(agg_ptr, members, r) */
+int uaamg_k_restrict(int nc, const int *agg_ptr, const int *members, const double *r, double *out, void *stream);
+/* K/numba_backend.py:288-294  prolongate_add(v2a, e_coarse, x) */
+int uaamg_k_prolongate_add(int n, const int *v2a, const double *e_coarse, const double *x, double *out,
+                           void *stream);
+/* K/numba_backend.py:297-310  smooth_sweeps (x is not modified; result in out) */
+int uaamg_k_smooth_sweeps(int n, const int *row_ptr, const int *col, const double *val, const double *inv_m,
+                          const double *x, const double *b, int sweeps, double *out, void *stream);
+
+/* aggregate(A, config) on device (U/aggregation.py:172-203): writes
+ * vertex_to_agg[n] and coarse_vertex_of_agg[*n_coarse] (caller buffers of
+ * size n).  size_cap <= 0 means unlimited. */
+int uaamg_aggregate(int n, const int *row_ptr, const int *col, const double *val, uint64_t seed, int max_passes,
+                    int64_t size_cap, int *vertex_to_agg, int *seeds, int *n_coarse, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* drivers                                                              */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int64_t size_cap;       /* <= 0: unlimited (AggregationConfig.size_cap=None) */
+    uint64_t seed;          /* AggregationConfig.seed                            */
+    int max_passes;         /* AggregationConfig.max_passes (20)                 */
+    int passes_per_level;   /* AggregationConfig.passes_per_level (1 or 2)       */
+    int n0;                 /* setup(n0=100)                                     */
+    int max_levels;         /* setup(max_levels=20)                              */
+    int singular;           /* -1 auto (detect_singular), 0/1 forced             */
+} uaamg_setup_params;
+
+/* U/hierarchy.py:120-153.  Matrix arrays are device pointers, copied into
+ * the hierarchy.  Returns UAAMG_ESETUP on stagnation (message as the
+ * reference's SetupError). */
+int uaamg_setup(int n, int64_t nnz, const int *row_ptr, const int *col, const double *val,
+                const uaamg_setup_params *params, uaamg_hierarchy **out, void *stream);
+void uaamg_hierarchy_free(uaamg_hierarchy *h);
+
+typedef struct {
+    int n_levels;
+    int singular;
+    double grid_complexity;
+    double operator_complexity;
+    double setup_seconds;   /* device time of the last setup (CUDA events) */
+} uaamg_hierarchy_info;
+int uaamg_hierarchy_get_info(const uaamg_hierarchy *h, uaamg_hierarchy_info *info);
+
+/* Device views of level l (valid while h lives).  v2a/seeds/agg_ptr/members
+ * are NULL on the coarsest level (n_coarse = 0). */
+typedef struct {
+    int n;
+    int64_t nnz;
+    const int *row_ptr;
+    const int *col;
+    const double *val;
+    int n_coarse;
+    const int *vertex_to_agg;
+    const int *coarse_vertex_of_agg;
+    const int *agg_ptr;   /* members_csr (U/aggregation.py:70-77) */
+    const int *members;
+} uaamg_level_view;
+int uaamg_hierarchy_level(const uaamg_hierarchy *h, int level, uaamg_level_view *view);
+
+typedef struct {
+    int kcycle;              /* CycleSpec.kind: 1 kcycle, 0 vcycle           */
+    int inner_krylov_steps;  /* CycleSpec.inner_krylov_steps (2)            */
+    int pre_sweeps;          /* CycleSpec.pre_sweeps (1)                     */
+    int post_sweeps;         /* CycleSpec.post_sweeps (1)                    */
+    int smoother_l1;         /* Smoother.kind: 1 "l1", 0 "jacobi"            */
+    double omega;            /* Smoother.omega (2/3)                         */
+    double tol;              /* npcg_solve tol                                */
+    int max_iters;           /* npcg_solve max_iters                          */
+    int use_graphs;          /* 1: replay one CUDA graph per iteration        */
+    int profile_level0;      /* 1: time level-0 smoother kernels (events)     */
+} uaamg_solve_params;
+
+typedef struct {
+    int iterations;
+    int converged;
+    int status;              /* 0 ok, UAAMG_ENUMERICAL on breakdown etc.      */
+    double solve_seconds;    /* device time (CUDA events)                     */
+    /* level-0 hot-kernel timing when profile_level0 = 1 */
+    int64_t l0_kernel_launches;
+    double l0_kernel_seconds;
+    double l0_kernel_bytes;  /* algorithmic bytes over those launches          */
+} uaamg_solve_result;
+
+/* U/solvers.py:190-255.  b, x0 (may be NULL), x are device pointers of
+ * length n; history (device or host, see history_on_host) receives
+ * iterations+1 relative residuals (capacity max_iters+1). */
+int uaamg_npcg_solve(uaamg_hierarchy *h, const uaamg_solve_params *p, const double *b, const double *x0, double *x,
+                     double *history_host, uaamg_solve_result *res, void *stream);
+
+/* Level-0 hot-kernel timing of the last solve run with profile_level0 = 1:
+ * device seconds summed over the working iterations (CUDA events captured
+ * around the kernels inside the iteration graph) and algorithmic bytes per
+ * launch, for [0] residual, [1] fused prolongation + l1/Jacobi post-sweep,
+ * [2] direction SpMV (+ dots).  *count = iterations timed. */
+int uaamg_solve_profile(const uaamg_hierarchy *h, double *seconds3, double *bytes3, int64_t *count);
+
+/* U/solvers.py:128-157: one cycle on level `level` from a zero guess. */
+int uaamg_cycle(uaamg_hierarchy *h, const uaamg_solve_params *p, int level, const double *b, double *x,
+                void *stream);
+
+/* smooth(a, smoother, x, b, sweeps) for level `level` of h (U/solvers.py:84-91) */
+int uaamg_smooth(uaamg_hierarchy *h, const uaamg_solve_params *p, int level, const double *x, const double *b,
+                 int sweeps, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UAAMG_B200_H */

@@ -1,0 +1,28 @@
+"""B200-native unsmoothed-aggregation AMG (arXiv 1302.2547) -- setup/solve path.
+
+Drop-in for the setup/solve subset of the reference package ``uaamg``
+(/root/reference/pkg/src/uaamg/__init__.py:3-38): same names, signatures,
+defaults and exception types.  All numerical work runs in hand-written
+sm_100a CUDA kernels in ``libuaamg_b200.so`` (C ABI: include/uaamg_b200.h);
+there is no CPU fallback.
+"""
+
+from .aggregation import (Aggregation, AggregationConfig, AggregationError, aggregate, compose,
+                          quasi_random_scores, select_coarse_vertices, singleton_aggregation)
+from .device import DeviceCSR
+from .hierarchy import CoarseSolver, Hierarchy, Level, SetupError, detect_singular, galerkin_coarse, setup
+from .solvers import (CycleSpec, NumericalError, Smoother, SolveReport, cycle, npcg_solve, prolongate_add,
+                      restrict, smooth, smoother_inverse_diag)
+from .sparse import SparseFormatError, SparseMatrix
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Aggregation", "AggregationConfig", "AggregationError", "aggregate", "compose", "quasi_random_scores",
+    "select_coarse_vertices", "singleton_aggregation",
+    "CoarseSolver", "Hierarchy", "Level", "SetupError", "detect_singular", "galerkin_coarse", "setup",
+    "CycleSpec", "NumericalError", "Smoother", "SolveReport", "cycle", "npcg_solve", "prolongate_add", "restrict",
+    "smooth", "smoother_inverse_diag",
+    "SparseMatrix", "SparseFormatError", "DeviceCSR",
+    "__version__",
+]

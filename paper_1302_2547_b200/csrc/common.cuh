@@ -1,0 +1,153 @@
+// common.cuh -- shared types and device helpers for the B200 UA-AMG library.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "uaamg_b200.h"
+
+namespace uaamg {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define UA_CK(x)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw ::uaamg::Error(UAAMG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" \
+                                                  __FILE__ ":" + std::to_string(__LINE__) + ")");     \
+    } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+
+// Every library kernel launch goes through this (launch accounting + error check).
+#define UA_LAUNCH(kernel, grid, block, smem, stream, ...)                        \
+    do {                                                                         \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+        ::uaamg::g_launches.fetch_add(1, std::memory_order_relaxed);             \
+        UA_CK(cudaGetLastError());                                               \
+    } while (0)
+
+// ---------------------------------------------------------------- device memory
+// Stream-ordered allocation from the device's default memory pool.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = 0;
+    DBuf() = default;
+    DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) UA_CK(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { release(); }
+    T* get() const { return p; }
+};
+
+// ---------------------------------------------------------------- CSR views
+struct Csr {
+    int n = 0;            // rows (square)
+    int nnz = 0;
+    const int* rp = nullptr;
+    const int* ci = nullptr;
+    const double* av = nullptr;
+};
+
+// Row-block partition for the smem-staged kernels (see csr_stream.cuh).
+struct Blocks {
+    int nb = 0;
+    const int* start = nullptr;  // nb+1 entries, start[nb] = n
+};
+
+// ---------------------------------------------------------------- constants
+constexpr int kThreads = 256;           // staged kernels: threads per block
+constexpr int kRowsPerBlock = 256;      // max rows per row block
+constexpr int kStageCap = 2048;         // products staged per block (16 KB fp64)
+constexpr int kStageHalf = kStageCap / 2;
+constexpr int kNumSMs = 148;            // B200
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum (fixed shuffle tree + fixed smem order).  All
+// threads of the block must call it; result valid in every thread.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sm /* >= NT/32 + 1 */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sm[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = (lane < NT / 32) ? sm[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) sm[NT / 32] = t;
+    }
+    __syncthreads();
+    return sm[NT / 32];
+}
+
+// Deterministic grid-wide reduction of K doubles per thread: block sums go
+// to partials[k*nb + block]; the last block to arrive (atomic ticket) sums
+// the partials in block order and calls fin(tot) on thread 0, then rearms
+// the ticket.  Must be called by all threads of every block of the launch.
+template <int K, class F>
+__device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* partials, unsigned* ticket, F&& fin) {
+    __shared__ double sm[kThreads / 32 + 1];
+    __shared__ bool last;
+    double tot[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = block_sum<kThreads>(v[k], sm);
+    const int nb = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) partials[k * nb + blockIdx.x] = tot[k];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)(nb - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nb; b += kThreads) s += __ldcg(partials + k * nb + b);
+        tot[k] = block_sum<kThreads>(s, sm);
+    }
+    if (threadIdx.x == 0) {
+        fin(tot);
+        __threadfence();
+        *ticket = 0u;
+    }
+}
+
+}  // namespace uaamg

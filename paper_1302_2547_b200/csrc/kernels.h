@@ -1,0 +1,101 @@
+// kernels.h -- host-side launchers for the device kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace uaamg {
+
+constexpr int kMaxInner = 16;
+
+// Per-level state of one inner flexible-CG invocation (U/solvers.py:160-187).
+// Only one FCG per level is active at a time, so one slot per level.
+struct FcgState {
+    double bnorm;                 // ||b|| of the FCG right-hand side
+    double beta, alpha, pap, pr;
+    double rnorm;
+    double sum;                   // scratch: sum for mean projection
+    int gate[kMaxInner + 1];      // gate[s]: step s runs (cycle + direction)
+    int upd[kMaxInner];           // upd[s]: step s updated x, r
+    int err;                      // singular incompatibility flag
+};
+
+// Outer NPCG state (U/solvers.py:190-255)
+struct NpcgState {
+    double bnorm, beta, alpha, pap, pr, last_rel, tol;
+    double sum;
+    int active;       // iteration gate (not done)
+    int have_prev;    // p_prev/ap_prev valid (restart clears)
+    int up;           // consecutive residual increases
+    int iters;
+    int status;       // 0 ok, 1 breakdown, 2 incompatible rhs
+    int max_iters;
+    int err_level;
+    double err_drift;
+};
+
+// Reduction scratch shared by all reductions on one stream (sequential use).
+struct RedScratch {
+    double* partials;   // >= kMaxRedBlocks * 4
+    unsigned* ticket;
+};
+constexpr int kMaxRedBlocks = 1 << 16;
+
+// ---- staged CSR operations (csr_stream.cuh) ----
+void launch_spmv(const Csr& A, const Blocks& B, const double* x, double* y, cudaStream_t s);
+// r = b - A x, x given (xmode 2) or implicit one sweep from zero (xmode 1) or zero (xmode 0)
+void launch_residual(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,
+                     const double* x, double* r, const int* gate, cudaStream_t s);
+// one Jacobi/l1 sweep: out = x + invm (b - A x), x from a vector
+void launch_sweep_vec(const Csr& A, const Blocks& B, const double* invm, const double* b, const double* x,
+                      double* out, const int* gate, cudaStream_t s);
+// prolongation fused into a sweep: x = xpre + ec[v2a] built on the fly
+void launch_sweep_up(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,
+                     const double* xpre, const int* v2a, const double* ec, const int* ec_valid, double* out,
+                     const int* gate, cudaStream_t s);
+// restriction as a unit-valued staged row sum over members_csr
+void launch_restrict(int nc, const int* agg_ptr, const int* members, const Blocks& MB, const double* r,
+                     double* rc, const int* gate, cudaStream_t s);
+// direction + SpMV + dots, FCG flavour: p = z (+ beta pprev), ap = A p, pap, pr -> alpha, upd[step]
+void launch_dir_fcg(const Csr& A, const Blocks& B, const double* z, const double* pprev, int have_prev,
+                    const double* r, double* p, double* ap, FcgState* st, int step, RedScratch rs,
+                    cudaStream_t s);
+// NPCG flavour (have_prev / breakdown handled on device)
+void launch_dir_npcg(const Csr& A, const Blocks& B, const double* z, const double* pprev, const double* r,
+                     double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);
+
+// ---- elementwise / reductions ----
+void launch_inv_diag(const Csr& A, int l1, double omega, double* invm, int* bad_row, cudaStream_t s);
+void launch_xpre1(int n, const double* invm, const double* b, double* x, const int* gate, cudaStream_t s);
+void launch_prolongate(int n, int xmode, const double* invm, const double* b, const double* xpre, const int* v2a,
+                       const double* ec, const int* ec_valid, double* out, const int* gate, cudaStream_t s);
+// ||b|| -> st->bnorm, gate[0] = parent && !(||b|| <= 1e-14 ||b||)
+void launch_fcg_begin(int n, const double* b, const int* parent_gate, FcgState* st, RedScratch rs, cudaStream_t s);
+// beta = -(z.apprev)/(pprev.apprev) into *beta (gate: flag pointer)
+void launch_beta(int n, const double* z, const double* pprev, const double* apprev, double* beta, const int* gate,
+                 const int* gate2, RedScratch rs, cudaStream_t s);
+// x (+)= alpha p, r_out = r_in - alpha ap, rnorm -> gate[step+1]
+void launch_fcg_update(int n, int step, double* x, const double* p, const double* r_in, double* r_out,
+                       const double* ap, FcgState* st, int singular, RedScratch rs, cudaStream_t s);
+void launch_npcg_update(int n, double* x, const double* p, double* r, const double* ap, NpcgState* st,
+                        double* history, int singular, RedScratch rs, cudaStream_t s);
+// singular helpers: v -= mean(v)   (U/solvers.py:112-113)
+void launch_project_mean(int n, double* v, double* sum_slot, const int* gate, RedScratch rs, cudaStream_t s);
+// compatibility check + projection into out (U/solvers.py:116-125); flags st_err on drift
+void launch_check_compatible(int n, const double* b, double* out, int* err_flag, double* sum_slot,
+                             const int* gate, int level, RedScratch rs, cudaStream_t s);
+// dense coarsest solve x = Minv b
+void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, cudaStream_t s);
+// ||v||_2 on device into *out (plain, ungated)
+void launch_norm(int n, const double* v, double* out, RedScratch rs, cudaStream_t s);
+// NPCG init: bnorm, history[0], active
+void launch_npcg_init(int n, const double* b, const double* r, NpcgState* st, double* history, RedScratch rs,
+                      cudaStream_t s);
+void launch_copy(int n, const double* src, double* dst, cudaStream_t s);
+void launch_axpby_init(int n, const double* b, const double* ax, double* r, cudaStream_t s);  // r = b - ax
+
+// ---- setup kernels (kernels_setup.cu) ----
+void launch_degrees(const Csr& A, int* deg, cudaStream_t s);
+void launch_scores(const Csr& A, const int* deg, uint64_t seed, int64_t pass_idx, double* scores, cudaStream_t s);
+void launch_hash_u01(uint64_t seed, int64_t pass_idx, const int64_t* idx, int64_t m, double* out, cudaStream_t s);
+void launch_diag(const Csr& A, int l1, double* out, cudaStream_t s);
+
+}  // namespace uaamg

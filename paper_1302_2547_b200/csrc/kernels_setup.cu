@@ -1,0 +1,939 @@
+// kernels_setup.cu -- setup-phase kernels: counter hash + quasi-random
+// scores, distance-3 MIS selection and claim as two max-hops over A (no A^2),
+// conflict-free aggregate admission, renumbering by ascending seed,
+// members_csr, Galerkin coarse operator as an exact-order segmented
+// sum-by-aggregate-pair, dense coarsest factorization.
+//
+// Reference: U/aggregation.py:130-203, U/hierarchy.py:22-65,
+// K/numba_backend.py:14-44 (hash), :100-111 (scores), :145-273.
+#include <cub/cub.cuh>
+
+#include "setup.h"
+
+namespace uaamg {
+
+// ============================================================ hash + scores
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t pass_base(uint64_t seed, int64_t pass_idx) {
+    uint64_t z = seed ^ (0xA0761D6478BD642Full * (uint64_t)(pass_idx + 1));
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double hash_unit(uint64_t base, int64_t i) {
+    const uint64_t z = mix64(mix64(base + (uint64_t)i * 0x9E3779B97F4A7C15ull));
+    return __dmul_rn((double)(z >> 11), 1.0 / 9007199254740992.0);
+}
+
+__global__ void k_hash_u01(uint64_t base, const int64_t* idx, int64_t m, double* out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = hash_unit(base, idx[k]);
+}
+void launch_hash_u01(uint64_t seed, int64_t pass_idx, const int64_t* idx, int64_t m, double* out, cudaStream_t s) {
+    if (m == 0) return;
+    UA_LAUNCH(k_hash_u01, cdiv(m, 256) > 4096 ? 4096 : cdiv(m, 256), 256, 0, s, pass_base(seed, pass_idx), idx, m,
+              out);
+}
+
+// structural off-diagonal count (K/numba_backend.py:87-97)
+__global__ void k_degrees(Csr A, int* deg) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        int d = 0;
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) d += (A.ci[k] != i);
+        deg[i] = d;
+    }
+}
+void launch_degrees(const Csr& A, int* deg, cudaStream_t s) {
+    UA_LAUNCH(k_degrees, cdiv(A.n, 256), 256, 0, s, A, deg);
+}
+
+// v_i = d_i + ((i mod 12) + u_i) / 12, in exactly that evaluation order
+// (K/numba_backend.py:110)
+__global__ void k_scores(int n, const int* deg, uint64_t base, double* s) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double u = hash_unit(base, i);
+        s[i] = __dadd_rn((double)deg[i], __ddiv_rn(__dadd_rn((double)(i % 12), u), 12.0));
+    }
+}
+void launch_scores(const Csr& A, const int* deg, uint64_t seed, int64_t pass_idx, double* scores, cudaStream_t s) {
+    UA_LAUNCH(k_scores, cdiv(A.n, 256), 256, 0, s, A.n, deg, pass_base(seed, pass_idx), scores);
+}
+
+// ============================================================ MIS / claim hops
+// key(j) = (s_j, -j): j beats i iff s_j > s_i or (s_j == s_i and j < i)
+__device__ __forceinline__ bool key_gt(double sa, int ia, double sb, int ib) {
+    return sa > sb || (sa == sb && ia < ib);
+}
+
+// vertex state: 0 unprocessed, 1 center of the current pass, 2 processed
+// hop 1: m[k] = max key over j in row k with (mode 0: state != 2, mode 1: state == 1)
+__global__ void k_hop1(Csr A, const double* __restrict__ s, const uint8_t* __restrict__ st, int mode,
+                       double* __restrict__ ms, int* __restrict__ mi) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < A.n; k += gridDim.x * blockDim.x) {
+        double bs = 0.0;
+        int bi = -1;
+        for (int e = A.rp[k]; e < A.rp[k + 1]; ++e) {
+            const int j = __ldg(A.ci + e);
+            const uint8_t sj = __ldg(st + j);
+            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
+            const double v = __ldg(s + j);
+            if (bi < 0 || key_gt(v, j, bs, bi)) { bs = v; bi = j; }
+        }
+        ms[k] = bs;
+        mi[k] = bi;
+    }
+}
+
+// hop 2, selection (K/numba_backend.py:175-193): unprocessed i is a center
+// iff no unprocessed j != i within distance 2 has a larger key.
+__global__ void k_select(Csr A, const double* __restrict__ s, uint8_t* st, const double* __restrict__ ms,
+                         const int* __restrict__ mi, int* n_centers) {
+    int local = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        if (st[i] != 0) continue;
+        double bs = 0.0;
+        int bi = -1;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const int k = __ldg(A.ci + e);
+            const int c = __ldg(mi + k);
+            if (c < 0) continue;
+            const double v = __ldg(ms + k);
+            if (bi < 0 || key_gt(v, c, bs, bi)) { bs = v; bi = c; }
+        }
+        const double si = s[i];
+        if (bi < 0 || bi == i || key_gt(si, i, bs, bi)) {
+            st[i] = 1;
+            ++local;
+        }
+    }
+    if (local) atomicAdd(n_centers, local);
+}
+
+// hop 2, claim (K/numba_backend.py:196-220): owner = best center within
+// distance 2 if its score >= own score, centers own themselves.
+__global__ void k_claim(Csr A, const double* __restrict__ s, const uint8_t* __restrict__ st,
+                        const double* __restrict__ ms, const int* __restrict__ mi, int* owner) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x) {
+        const uint8_t sj = st[j];
+        if (sj == 1) { owner[j] = j; continue; }
+        if (sj == 2) { owner[j] = -1; continue; }
+        double bs = 0.0;
+        int bi = -1;
+        for (int e = A.rp[j]; e < A.rp[j + 1]; ++e) {
+            const int k = __ldg(A.ci + e);
+            const int c = __ldg(mi + k);
+            if (c < 0) continue;
+            const double v = __ldg(ms + k);
+            if (bi < 0 || key_gt(v, c, bs, bi)) { bs = v; bi = c; }
+        }
+        owner[j] = (bi >= 0 && !(bs < s[j])) ? bi : -1;
+    }
+}
+
+// explicit-pattern variants (kernel table: pattern = A^2)
+__global__ void k_select_pattern(Csr P, const double* s, const uint8_t* processed, uint8_t* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        if (processed[i]) { out[i] = 0; continue; }
+        bool ok = true;
+        const double si = s[i];
+        for (int e = P.rp[i]; e < P.rp[i + 1]; ++e) {
+            const int j = P.ci[e];
+            if (j == i || processed[j]) continue;
+            if (!key_gt(si, i, s[j], j)) { ok = false; break; }
+        }
+        out[i] = ok;
+    }
+}
+__global__ void k_claim_pattern(Csr P, const double* s, const uint8_t* processed, const uint8_t* is_center,
+                                int* owner) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.n; j += gridDim.x * blockDim.x) {
+        if (is_center[j]) { owner[j] = j; continue; }
+        owner[j] = -1;
+        if (processed[j]) continue;
+        int best = -1;
+        double bs = 0.0;
+        const double sj = s[j];
+        for (int e = P.rp[j]; e < P.rp[j + 1]; ++e) {
+            const int i = P.ci[e];
+            if (!is_center[i]) continue;
+            const double si = s[i];
+            if (si < sj) continue;
+            if (best == -1 || key_gt(si, i, bs, best)) { best = i; bs = si; }
+        }
+        owner[j] = best;
+    }
+}
+
+// ============================================================ admission
+// Uncapped (size_cap=None): the reference's repeated strongest-first sweeps
+// (K/numba_backend.py:235-273) admit exactly the bucket vertices connected to
+// the center through admitted bucket vertices, independent of sweep order.
+// That fixpoint is computed here by monotone label propagation.
+__global__ void k_admit_init(int n, const uint8_t* st, const int* owner, uint8_t* adm) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        adm[j] = (st[j] == 1);
+}
+__global__ void k_admit_step(Csr A, const int* __restrict__ owner, uint8_t* adm, int* changed) {
+    int local = 0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x) {
+        const int c = owner[j];
+        if (c < 0 || c == j || adm[j]) continue;
+        for (int e = A.rp[j]; e < A.rp[j + 1]; ++e) {
+            const int nb = __ldg(A.ci + e);
+            if (((volatile uint8_t*)adm)[nb] && __ldg(owner + nb) == c) {
+                adm[j] = 1;
+                local = 1;
+                break;
+            }
+        }
+    }
+    if (local) atomicOr(changed, 1);
+}
+// commit: admitted vertices and centers become processed with their seed
+__global__ void k_admit_commit(int n, uint8_t* st, const int* owner, const uint8_t* adm, int* seed_of,
+                               int* remaining) {
+    int local = 0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint8_t sj = st[j];
+        if (sj == 1 || (sj == 0 && adm[j])) {
+            seed_of[j] = owner[j];
+            st[j] = 2;
+        } else if (sj == 0) {
+            ++local;
+        }
+    }
+    if (local) atomicAdd(remaining, local);
+}
+
+// Capped: per-center sequential greedy exactly as the reference (bucket in
+// ascending vertex order, candidates by descending |A_cj| stable, sweeps).
+__global__ void k_bucket_count(int n, const uint8_t* st, const int* owner, int* cnt) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int c = owner[j];
+        if (c >= 0 && st[j] == 0) atomicAdd(cnt + c, 1);
+    }
+}
+__global__ void k_bucket_fill(int n, const uint8_t* st, const int* owner, const int* bptr, int* cursor, int* bjs) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int c = owner[j];
+        if (c >= 0 && st[j] == 0) bjs[bptr[c] + atomicAdd(cursor + c, 1)] = j;
+    }
+}
+__device__ int lower_bound_i(const int* v, int lo, int hi, int key) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+// one thread per center; scratch ord/adm per bucket slot
+__global__ void k_admit_capped(Csr A, int n, const uint8_t* st, const int* bptr, int* bjs, int* ord, double* w,
+                               uint8_t* admf, long long cap, int* seed_of, uint8_t* newly) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        if (st[c] != 1) continue;
+        const int lo = bptr[c], m = bptr[c + 1] - lo;
+        int* js = bjs + lo;
+        int* od = ord + lo;
+        double* wv = w + lo;
+        uint8_t* ad = admf + lo;
+        // ascending vertex order within the bucket (U/aggregation.py:157,164)
+        for (int a = 1; a < m; ++a) {
+            const int t = js[a];
+            int b = a - 1;
+            while (b >= 0 && js[b] > t) { js[b + 1] = js[b]; --b; }
+            js[b + 1] = t;
+        }
+        const int rs = A.rp[c], re = A.rp[c + 1];
+        for (int t = 0; t < m; ++t) {
+            const int pos = lower_bound_i(A.ci, rs, re, js[t]);
+            wv[t] = (pos < re && A.ci[pos] == js[t]) ? fabs(A.av[pos]) : 0.0;
+            ad[t] = 0;
+            // stable insertion by descending weight (mergesort of -w)
+            int b = t - 1;
+            while (b >= 0 && wv[od[b]] < wv[t]) { od[b + 1] = od[b]; --b; }
+            od[b + 1] = t;
+        }
+        long long count = 1;
+        bool progress = true;
+        while (progress && count < cap) {
+            progress = false;
+            for (int t = 0; t < m; ++t) {
+                if (count >= cap) break;
+                const int id = od[t];
+                if (ad[id]) continue;
+                const int j = js[id];
+                bool conn = false;
+                for (int e = A.rp[j]; e < A.rp[j + 1]; ++e) {
+                    const int nb = A.ci[e];
+                    if (nb == c) { conn = true; break; }
+                    const int pos = lower_bound_i(js, 0, m, nb);
+                    if (pos < m && js[pos] == nb && ad[pos]) { conn = true; break; }
+                }
+                if (conn) {
+                    ad[id] = 1;
+                    seed_of[j] = c;
+                    newly[j] = 1;
+                    ++count;
+                    progress = true;
+                }
+            }
+        }
+        seed_of[c] = c;
+    }
+}
+__global__ void k_capped_commit(int n, uint8_t* st, uint8_t* newly, int* remaining) {
+    int local = 0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        if (st[j] == 1 || newly[j]) { st[j] = 2; newly[j] = 0; }
+        else if (st[j] == 0) ++local;
+    }
+    if (local) atomicAdd(remaining, local);
+}
+
+// ============================================================ renumbering
+// leftovers become singletons (U/aggregation.py:195-198); seed flags
+__global__ void k_finish_seeds(int n, const uint8_t* st, int* seed_of, int* flag) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        if (st[v] != 2) seed_of[v] = v;
+        flag[v] = (seed_of[v] == v);
+    }
+}
+// new id = rank of the seed among all seeds (U/aggregation.py:199-203)
+__global__ void k_renumber(int n, const int* seed_of, const int* flag, const int* rank, int* v2a, int* seeds) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        if (flag[v]) seeds[rank[v]] = v;
+        v2a[v] = rank[seed_of[v]];
+    }
+}
+
+// ============================================================ members_csr
+__global__ void k_iota(int n, int* v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+__global__ void k_seg_starts(int n, int nc, const int* sorted_keys, int* ptr) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int k = sorted_keys[i];
+        if (i == 0 || sorted_keys[i - 1] != k) ptr[k] = i;
+        if (i == n - 1) ptr[nc] = n;
+    }
+}
+
+// ============================================================ row blocks
+__global__ void k_block_flags(int n, const int* rp, int* flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int len = rp[i + 1] - rp[i];
+        bool f = (i % kRowsPerBlock) == 0 || len > kStageHalf;
+        if (!f) {
+            const int lp = rp[i] - rp[i - 1];
+            f = lp > kStageHalf || (rp[i] / kStageHalf) != (rp[i - 1] / kStageHalf);
+        }
+        flag[i] = f;
+    }
+}
+__global__ void k_block_scatter(int n, const int* flag, const int* pos, int* start, int nb) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (flag[i]) start[pos[i]] = i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) start[nb] = n;
+}
+
+// ============================================================ Galerkin
+// stream length per aggregate: sum of its members' row lengths
+__global__ void k_stream_len(int nc, const int* agg_ptr, const int* members, const int* rp, int* slen) {
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+        int s = 0;
+        for (int q = agg_ptr[I]; q < agg_ptr[I + 1]; ++q) {
+            const int m = members[q];
+            s += rp[m + 1] - rp[m];
+        }
+        slen[I] = s;
+    }
+}
+
+__device__ __forceinline__ unsigned hslot(int key, int cap) { return ((unsigned)key * 2654435761u) % (unsigned)cap; }
+
+// Phase A: one warp per aggregate I accumulates its coarse row in an
+// open-addressing table at hkey/hval[2*soff[I] .. +2*slen[I]).  The stream
+// (members ascending, each row's entries ascending) is consumed 32 entries
+// at a time; lanes with equal J are grouped with __match_any_sync and the
+// lowest lane adds the group's values in lane order -- so every (I,J) sum is
+// sequential in the reference's stable-sort order (K/numba_backend.py:151-163).
+__global__ void k_galerkin_accum(Csr A, const int* __restrict__ v2a, int nc, const int* __restrict__ agg_ptr,
+                                 const int* __restrict__ members, const int* __restrict__ soff,
+                                 const int* __restrict__ slen, int* hkey, double* hval, int* cnt) {
+    __shared__ double wvals[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int I = blockIdx.x * 8 + wib;
+    if (I >= nc) return;
+    const int cap = 2 * slen[I];
+    int* K = hkey + 2 * (size_t)soff[I];
+    double* V = hval + 2 * (size_t)soff[I];
+    for (int q = agg_ptr[I]; q < agg_ptr[I + 1]; ++q) {
+        const int m = members[q];
+        const int e0 = A.rp[m], e1 = A.rp[m + 1];
+        for (int c0 = e0; c0 < e1; c0 += 32) {
+            const int e = c0 + lane;
+            const bool act = e < e1;
+            const unsigned am = __ballot_sync(0xffffffffu, act);
+            int J = -1;
+            double a = 0.0;
+            if (act) {
+                J = __ldg(v2a + __ldg(A.ci + e));
+                a = __ldg(A.av + e);
+            }
+            wvals[wib][lane] = a;
+            __syncwarp();
+            if (act) {
+                const unsigned g = __match_any_sync(am, J);
+                if ((__ffs(g) - 1) == lane) {
+                    unsigned slot = hslot(J, cap);
+                    while (true) {
+                        const int prev = atomicCAS(K + slot, -1, J);
+                        if (prev == -1 || prev == J) break;
+                        slot = (slot + 1 == (unsigned)cap) ? 0u : slot + 1;
+                    }
+                    volatile double* vs = V + slot;
+                    double acc = *vs;
+                    unsigned mm = g;
+                    while (mm) {
+                        const int l = __ffs(mm) - 1;
+                        acc = __dadd_rn(acc, wvals[wib][l]);
+                        mm &= mm - 1;
+                    }
+                    *vs = acc;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    // count nonzero sums (exact zeros dropped, K/numba_backend.py:164)
+    int c = 0;
+    for (int t = lane; t < cap; t += 32)
+        if (K[t] >= 0 && V[t] != 0.0) ++c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[I] = c;
+}
+
+// Phase C: write row I sorted by J (rank = number of smaller keys)
+__global__ void k_galerkin_emit(int nc, const int* __restrict__ soff, const int* __restrict__ slen,
+                                const int* __restrict__ hkey, const double* __restrict__ hval,
+                                const int* __restrict__ rp_c, int* col_c, double* val_c) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int I = blockIdx.x * 8 + wib;
+    if (I >= nc) return;
+    const int cap = 2 * slen[I];
+    const int* K = hkey + 2 * (size_t)soff[I];
+    const double* V = hval + 2 * (size_t)soff[I];
+    const int base = rp_c[I];
+    for (int t = lane; t < cap; t += 32) {
+        const int key = K[t];
+        if (key < 0 || V[t] == 0.0) continue;
+        int rank = 0;
+        for (int u = 0; u < cap; ++u) {
+            const int k2 = K[u];
+            rank += (k2 >= 0 && k2 < key && V[u] != 0.0);
+        }
+        col_c[base + rank] = key;
+        val_c[base + rank] = V[t];
+    }
+}
+
+// ============================================================ coarsest dense
+__global__ void k_densify(Csr A, double* D) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x)
+        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) D[(size_t)i * A.n + A.ci[k]] = A.av[k];
+}
+
+// in-place lower Cholesky (row-major, lower triangle), single block; flag on
+// a non-positive pivot (scipy cho_factor LinAlgError, U/hierarchy.py:47-51)
+__global__ void k_cholesky(int n, double* L, int* fail) {
+    __shared__ double piv;
+    for (int j = 0; j < n; ++j) {
+        if (threadIdx.x == 0) {
+            double s = L[(size_t)j * n + j];
+            for (int k = 0; k < j; ++k) s -= L[(size_t)j * n + k] * L[(size_t)j * n + k];
+            if (!(s > 0.0)) { *fail = 1; piv = 0.0; }
+            else { piv = sqrt(s); L[(size_t)j * n + j] = piv; }
+        }
+        __syncthreads();
+        if (piv == 0.0) return;
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            double s = L[(size_t)i * n + j];
+            for (int k = 0; k < j; ++k) s -= L[(size_t)i * n + k] * L[(size_t)j * n + k];
+            L[(size_t)i * n + j] = s / piv;
+        }
+        __syncthreads();
+    }
+}
+// inverse from the Cholesky factor: column c of A^{-1} per thread
+__global__ void k_chol_inverse(int n, const double* L, double* Minv, double* work) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double* y = work + (size_t)c * n;
+    for (int i = 0; i < n; ++i) {  // L y = e_c
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) s -= L[(size_t)i * n + k] * y[k];
+        y[i] = s / L[(size_t)i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {  // L^T x = y
+        double s = y[i];
+        for (int k = i + 1; k < n; ++k) s -= L[(size_t)k * n + i] * y[k];
+        y[i] = s / L[(size_t)i * n + i];
+    }
+    for (int i = 0; i < n; ++i) Minv[(size_t)i * n + c] = y[i];
+}
+
+// cyclic Jacobi eigen-decomposition (single block) for the singular /
+// indefinite fallback (numpy eigh, U/hierarchy.py:52-54)
+__global__ void k_jacobi_eigh(int n, double* A, double* V, int sweeps) {
+    __shared__ double cs, sn;
+    __shared__ int skip;
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) V[t] = ((t / n) == (t % n)) ? 1.0 : 0.0;
+    __syncthreads();
+    __shared__ double red[256];
+    for (int sw = 0; sw < sweeps; ++sw) {
+        // stop when the off-diagonal mass is negligible
+        double off = 0.0, tot = 0.0;
+        for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+            const double v = A[t] * A[t];
+            tot += v;
+            if ((t / n) != (t % n)) off += v;
+        }
+        red[threadIdx.x] = off;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double o = 0.0;
+            for (int k = 0; k < (int)blockDim.x; ++k) o += red[k];
+            red[0] = o;
+        }
+        __syncthreads();
+        const double offs = red[0];
+        __syncthreads();
+        red[threadIdx.x] = tot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double o = 0.0;
+            for (int k = 0; k < (int)blockDim.x; ++k) o += red[k];
+            red[0] = o;
+        }
+        __syncthreads();
+        const double tots = red[0];
+        __syncthreads();
+        if (offs <= 1e-30 * (tots > 0.0 ? tots : 1.0)) break;
+        for (int p = 0; p < n; ++p) {
+            for (int q = p + 1; q < n; ++q) {
+                if (threadIdx.x == 0) {
+                    const double apq = A[(size_t)p * n + q];
+                    skip = fabs(apq) < 1e-300;
+                    if (!skip) {
+                        const double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+                        const double th = (aqq - app) / (2.0 * apq);
+                        const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        cs = 1.0 / sqrt(t * t + 1.0);
+                        sn = t * cs;
+                    }
+                }
+                __syncthreads();
+                if (!skip) {
+                    const double c = cs, s = sn;
+                    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                        const double akp = A[(size_t)k * n + p], akq = A[(size_t)k * n + q];
+                        A[(size_t)k * n + p] = c * akp - s * akq;
+                        A[(size_t)k * n + q] = s * akp + c * akq;
+                    }
+                    __syncthreads();
+                    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                        const double apk = A[(size_t)p * n + k], aqk = A[(size_t)q * n + k];
+                        A[(size_t)p * n + k] = c * apk - s * aqk;
+                        A[(size_t)q * n + k] = s * apk + c * aqk;
+                        const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
+                        V[(size_t)k * n + p] = c * vkp - s * vkq;
+                        V[(size_t)k * n + q] = s * vkp + c * vkq;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+// pinv = V diag(inv) V^T with cut = 1e-12 * max(lambda_max, 0)
+__global__ void k_pinv(int n, const double* A, const double* V, double* M) {
+    __shared__ double lmax;
+    if (threadIdx.x == 0) {
+        double m = -1e300;
+        for (int k = 0; k < n; ++k) m = fmax(m, A[(size_t)k * n + k]);
+        lmax = m;
+    }
+    __syncthreads();
+    const double cut = 1e-12 * fmax(lmax, 0.0);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * n; t += gridDim.x * blockDim.x) {
+        const int i = t / n, j = t % n;
+        double s = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double w = A[(size_t)k * n + k];
+            if (w > cut) s += V[(size_t)i * n + k] * (1.0 / w) * V[(size_t)j * n + k];
+        }
+        M[t] = s;
+    }
+}
+
+// ============================================================ squared pattern (kernel table)
+__global__ void k_sq_count(Csr A, long long* cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        long long c = 0;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const int k = A.ci[e];
+            c += A.rp[k + 1] - A.rp[k];
+        }
+        cnt[i] = c;
+    }
+}
+__global__ void k_sq_expand(Csr A, const long long* off, unsigned long long* keys) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        long long p = off[i];
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const int k = A.ci[e];
+            for (int e2 = A.rp[k]; e2 < A.rp[k + 1]; ++e2)
+                keys[p++] = ((unsigned long long)i << 32) | (unsigned)A.ci[e2];
+        }
+    }
+}
+
+// ============================================================ host drivers
+static int grid_for(int n) { return std::max(1, std::min(cdiv(n, 256), 4 * kNumSMs)); }
+
+template <class T>
+static void exclusive_scan(const T* in, T* out, int n, cudaStream_t s) {
+    size_t tmp = 0;
+    UA_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
+    DBuf<char> t(tmp, s);
+    UA_CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, s));
+}
+
+void build_row_blocks(int n, const int* rp, DBuf<int>& start, int& nb, cudaStream_t s) {
+    if (n == 0) {
+        nb = 0;
+        start.alloc(1, s);
+        UA_CK(cudaMemsetAsync(start.p, 0, sizeof(int), s));
+        return;
+    }
+    DBuf<int> flag(n + 1, s), pos(n + 1, s);
+    UA_LAUNCH(k_block_flags, grid_for(n), 256, 0, s, n, rp, flag.p);
+    UA_CK(cudaMemsetAsync(flag.p + n, 0, sizeof(int), s));
+    exclusive_scan(flag.p, pos.p, n + 1, s);
+    int h_nb = 0;
+    UA_CK(cudaMemcpyAsync(&h_nb, pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    nb = h_nb;
+    start.alloc(nb + 1, s);
+    UA_LAUNCH(k_block_scatter, grid_for(n), 256, 0, s, n, flag.p, pos.p, start.p, nb);
+}
+
+// aggregate() on device.  state arrays are n-sized scratch.
+int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes, long long size_cap,
+                     int* v2a, int* seeds, cudaStream_t s, AggStats* stats) {
+    const int n = A.n;
+    if (n <= 0) throw Error(UAAMG_EAGG, "cannot aggregate an empty matrix");
+    const int G = grid_for(n);
+    DBuf<uint8_t> st(n, s), adm(n, s);
+    DBuf<double> sc(n, s), ms(n, s);
+    DBuf<int> mi(n, s), owner(n, s), seed_of(n, s), counters(4, s);
+    UA_CK(cudaMemsetAsync(st.p, 0, n, s));
+    UA_CK(cudaMemsetAsync(seed_of.p, 0xff, sizeof(int) * n, s));
+    int* h_cnt = nullptr;
+    UA_CK(cudaMallocHost(&h_cnt, 4 * sizeof(int)));
+    const bool capped = size_cap > 0;
+    DBuf<int> bcnt, bptr, bjs, ord, cursor;
+    DBuf<double> bw;
+    DBuf<uint8_t> badm, newly;
+    if (capped) {
+        bcnt.alloc(n + 1, s); bptr.alloc(n + 1, s); bjs.alloc(n, s); ord.alloc(n, s); cursor.alloc(n, s);
+        bw.alloc(n, s); badm.alloc(n, s); newly.alloc(n, s);
+        UA_CK(cudaMemsetAsync(newly.p, 0, n, s));
+    }
+    int passes = 0;
+    int remaining = n;
+    for (int pass = 0; pass < max_passes; ++pass) {
+        if (remaining == 0) break;  // U/aggregation.py:186
+        UA_CK(cudaMemsetAsync(counters.p, 0, 4 * sizeof(int), s));
+        launch_scores(A, deg, seed, pass, sc.p, s);
+        UA_LAUNCH(k_hop1, G, 256, 0, s, A, sc.p, st.p, 0, ms.p, mi.p);
+        UA_LAUNCH(k_select, G, 256, 0, s, A, sc.p, st.p, ms.p, mi.p, counters.p + 0);
+        UA_LAUNCH(k_hop1, G, 256, 0, s, A, sc.p, st.p, 1, ms.p, mi.p);
+        UA_LAUNCH(k_claim, G, 256, 0, s, A, sc.p, st.p, ms.p, mi.p, owner.p);
+        if (!capped) {
+            UA_LAUNCH(k_admit_init, G, 256, 0, s, n, st.p, owner.p, adm.p);
+            for (int it = 0; it < n + 1; ++it) {
+                UA_CK(cudaMemsetAsync(counters.p + 1, 0, sizeof(int), s));
+                UA_LAUNCH(k_admit_step, G, 256, 0, s, A, owner.p, adm.p, counters.p + 1);
+                UA_CK(cudaMemcpyAsync(h_cnt + 1, counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+                UA_CK(cudaStreamSynchronize(s));
+                if (h_cnt[1] == 0) break;
+            }
+            UA_LAUNCH(k_admit_commit, G, 256, 0, s, n, st.p, owner.p, adm.p, seed_of.p, counters.p + 2);
+        } else {
+            UA_CK(cudaMemsetAsync(bcnt.p, 0, sizeof(int) * (n + 1), s));
+            UA_CK(cudaMemsetAsync(cursor.p, 0, sizeof(int) * n, s));
+            UA_LAUNCH(k_bucket_count, G, 256, 0, s, n, st.p, owner.p, bcnt.p);
+            exclusive_scan(bcnt.p, bptr.p, n + 1, s);
+            UA_LAUNCH(k_bucket_fill, G, 256, 0, s, n, st.p, owner.p, bptr.p, cursor.p, bjs.p);
+            UA_LAUNCH(k_admit_capped, G, 256, 0, s, A, n, st.p, bptr.p, bjs.p, ord.p, bw.p, badm.p, size_cap,
+                      seed_of.p, newly.p);
+            UA_LAUNCH(k_capped_commit, G, 256, 0, s, n, st.p, newly.p, counters.p + 2);
+        }
+        UA_CK(cudaMemcpyAsync(h_cnt, counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        ++passes;
+        remaining = h_cnt[2];
+        if (h_cnt[0] == 0) break;  // no centers: cannot happen (U/aggregation.py:190)
+    }
+    cudaFreeHost(h_cnt);
+    // leftovers + renumber
+    DBuf<int> flag(n + 1, s), rank(n + 1, s);
+    UA_LAUNCH(k_finish_seeds, G, 256, 0, s, n, st.p, seed_of.p, flag.p);
+    UA_CK(cudaMemsetAsync(flag.p + n, 0, sizeof(int), s));
+    exclusive_scan(flag.p, rank.p, n + 1, s);
+    UA_LAUNCH(k_renumber, G, 256, 0, s, n, seed_of.p, flag.p, rank.p, v2a, seeds);
+    int nc = 0;
+    UA_CK(cudaMemcpyAsync(&nc, rank.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    if (stats) { stats->passes = passes; stats->leftover = remaining; }
+    return nc;
+}
+
+void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cudaStream_t s) {
+    DBuf<int> iota(n, s), keys_out(n, s);
+    UA_LAUNCH(k_iota, grid_for(n), 256, 0, s, n, iota.p);
+    int bits = 1;
+    while ((1ll << bits) < (long long)nc) ++bits;
+    size_t tmp = 0;
+    UA_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, v2a, keys_out.p, iota.p, members, n, 0, bits, s));
+    DBuf<char> t(tmp, s);
+    UA_CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, v2a, keys_out.p, iota.p, members, n, 0, bits, s));
+    UA_LAUNCH(k_seg_starts, grid_for(n), 256, 0, s, n, nc, keys_out.p, agg_ptr);
+}
+
+// Galerkin: returns nnz_c; allocates out arrays
+long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
+                          DBuf<int>& rp_c, DBuf<int>& ci_c, DBuf<double>& av_c, cudaStream_t s) {
+    DBuf<int> slen(nc + 1, s), soff(nc + 1, s), cnt(nc + 1, s);
+    UA_LAUNCH(k_stream_len, grid_for(nc), 256, 0, s, nc, agg_ptr, members, A.rp, slen.p);
+    UA_CK(cudaMemsetAsync(slen.p + nc, 0, sizeof(int), s));
+    exclusive_scan(slen.p, soff.p, nc + 1, s);
+    const size_t hsz = 2 * (size_t)std::max(A.nnz, 1);
+    DBuf<int> hkey(hsz, s);
+    DBuf<double> hval(hsz, s);
+    UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
+    UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
+    UA_LAUNCH(k_galerkin_accum, cdiv(nc, 8), 256, 0, s, A, v2a, nc, agg_ptr, members, soff.p, slen.p, hkey.p,
+              hval.p, cnt.p);
+    UA_CK(cudaMemsetAsync(cnt.p + nc, 0, sizeof(int), s));
+    rp_c.alloc(nc + 1, s);
+    exclusive_scan(cnt.p, rp_c.p, nc + 1, s);
+    int nnz_c = 0;
+    UA_CK(cudaMemcpyAsync(&nnz_c, rp_c.p + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    ci_c.alloc(std::max(nnz_c, 1), s);
+    av_c.alloc(std::max(nnz_c, 1), s);
+    UA_LAUNCH(k_galerkin_emit, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ci_c.p, av_c.p);
+    return nnz_c;
+}
+
+// coarsest: dense inverse (Cholesky) or eigen pseudo-inverse
+int device_coarse_factor(const Csr& A, bool singular, DBuf<double>& Minv, cudaStream_t s) {
+    const int n = A.n;
+    Minv.alloc((size_t)std::max(n, 1) * std::max(n, 1), s);
+    if (n == 0) return 0;
+    DBuf<double> D((size_t)n * n, s);
+    UA_CK(cudaMemsetAsync(D.p, 0, sizeof(double) * n * n, s));
+    UA_LAUNCH(k_densify, grid_for(n), 256, 0, s, A, D.p);
+    int mode = 2;
+    if (!singular) {
+        DBuf<double> L((size_t)n * n, s), work((size_t)n * n, s);
+        DBuf<int> fail(1, s);
+        UA_CK(cudaMemsetAsync(fail.p, 0, sizeof(int), s));
+        UA_CK(cudaMemcpyAsync(L.p, D.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+        UA_LAUNCH(k_cholesky, 1, 1024, 0, s, n, L.p, fail.p);
+        int h_fail = 0;
+        UA_CK(cudaMemcpyAsync(&h_fail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        if (!h_fail) {
+            UA_LAUNCH(k_chol_inverse, cdiv(n, 128), 128, 0, s, n, L.p, Minv.p, work.p);
+            mode = 1;
+        }
+    }
+    if (mode == 2) {
+        DBuf<double> V((size_t)n * n, s);
+        UA_LAUNCH(k_jacobi_eigh, 1, 256, 0, s, n, D.p, V.p, 60);
+        UA_LAUNCH(k_pinv, std::min(cdiv((long long)n * n, 256), 1024), 256, 0, s, n, D.p, V.p, Minv.p);
+    }
+    UA_CK(cudaStreamSynchronize(s));
+    return mode;
+}
+
+// explicit pattern selection / claim (kernel table)
+void launch_select_pattern(const Csr& P, const double* s_, const uint8_t* processed, uint8_t* out, cudaStream_t s) {
+    UA_LAUNCH(k_select_pattern, grid_for(P.n), 256, 0, s, P, s_, processed, out);
+}
+void launch_claim_pattern(const Csr& P, const double* s_, const uint8_t* processed, const uint8_t* is_center,
+                          int* owner, cudaStream_t s) {
+    UA_LAUNCH(k_claim_pattern, grid_for(P.n), 256, 0, s, P, s_, processed, is_center, owner);
+}
+
+// 2-hop selection/claim for the kernel table: processed/is_center -> state
+__global__ void k_state_from(int n, const uint8_t* processed, const uint8_t* is_center, uint8_t* st) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        st[i] = processed[i] ? 2 : ((is_center && is_center[i]) ? 1 : 0);
+}
+__global__ void k_state_to_center(int n, const uint8_t* st, uint8_t* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = st[i] == 1;
+}
+void select_2hop(const Csr& A, const double* sc, const uint8_t* processed, uint8_t* out, cudaStream_t s) {
+    const int n = A.n, G = grid_for(n);
+    DBuf<uint8_t> st(n, s);
+    DBuf<double> ms(n, s);
+    DBuf<int> mi(n, s), cnt(1, s);
+    UA_CK(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+    UA_LAUNCH(k_state_from, G, 256, 0, s, n, processed, (const uint8_t*)nullptr, st.p);
+    UA_LAUNCH(k_hop1, G, 256, 0, s, A, sc, st.p, 0, ms.p, mi.p);
+    UA_LAUNCH(k_select, G, 256, 0, s, A, sc, st.p, ms.p, mi.p, cnt.p);
+    UA_LAUNCH(k_state_to_center, G, 256, 0, s, n, st.p, out);
+}
+void claim_2hop(const Csr& A, const double* sc, const uint8_t* processed, const uint8_t* is_center, int* owner,
+                cudaStream_t s) {
+    const int n = A.n, G = grid_for(n);
+    DBuf<uint8_t> st(n, s);
+    DBuf<double> ms(n, s);
+    DBuf<int> mi(n, s);
+    UA_LAUNCH(k_state_from, G, 256, 0, s, n, processed, is_center, st.p);
+    UA_LAUNCH(k_hop1, G, 256, 0, s, A, sc, st.p, 1, ms.p, mi.p);
+    UA_LAUNCH(k_claim, G, 256, 0, s, A, sc, st.p, ms.p, mi.p, owner);
+}
+
+// admit_members with caller-built buckets (kernel table): sequential greedy
+// per center, reusing k_admit_capped's logic through a bucket-per-center view
+__global__ void k_admit_table(Csr A, int nctr, const int* centers, const int* bptr, const int* bjs, long long cap,
+                              uint8_t* processed, int* v2a, int agg_base, int* ord, double* w, uint8_t* admf) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nctr; b += gridDim.x * blockDim.x) {
+        const int c = centers[b];
+        const int agg = agg_base + b;
+        v2a[c] = agg;
+        processed[c] = 1;
+        const int lo = bptr[b], m = bptr[b + 1] - lo;
+        const int* js = bjs + lo;
+        int* od = ord + lo;
+        double* wv = w + lo;
+        uint8_t* ad = admf + lo;
+        const int rs = A.rp[c], re = A.rp[c + 1];
+        for (int t = 0; t < m; ++t) {
+            const int pos = lower_bound_i(A.ci, rs, re, js[t]);
+            wv[t] = (pos < re && A.ci[pos] == js[t]) ? fabs(A.av[pos]) : 0.0;
+            ad[t] = 0;
+            int q = t - 1;
+            while (q >= 0 && wv[od[q]] < wv[t]) { od[q + 1] = od[q]; --q; }
+            od[q + 1] = t;
+        }
+        long long count = 1;
+        bool progress = true;
+        while (progress && count < cap) {
+            progress = false;
+            for (int t = 0; t < m; ++t) {
+                if (count >= cap) break;
+                const int id = od[t];
+                if (ad[id]) continue;
+                const int j = js[id];
+                bool conn = false;
+                for (int e = A.rp[j]; e < A.rp[j + 1]; ++e) {
+                    const int nb = A.ci[e];
+                    if (nb == c) { conn = true; break; }
+                    const int pos = lower_bound_i(js, 0, m, nb);
+                    if (pos < m && js[pos] == nb && ad[pos]) { conn = true; break; }
+                }
+                if (conn) {
+                    ad[id] = 1;
+                    v2a[j] = agg;
+                    processed[j] = 1;
+                    ++count;
+                    progress = true;
+                }
+            }
+        }
+    }
+}
+void admit_table(const Csr& A, int nctr, const int* centers, const int* bptr, const int* bjs, long long cap,
+                 uint8_t* processed, int* v2a, int agg_base, int total_bucket, cudaStream_t s) {
+    const int m = std::max(total_bucket, 1);
+    DBuf<int> ord(m, s);
+    DBuf<double> w(m, s);
+    DBuf<uint8_t> adm(m, s);
+    UA_LAUNCH(k_admit_table, grid_for(nctr), 256, 0, s, A, nctr, centers, bptr, bjs, cap, processed, v2a, agg_base,
+              ord.p, w.p, adm.p);
+}
+
+long long squared_pattern(const Csr& A, int* out_ptr, int* out_idx, cudaStream_t s) {
+    const int n = A.n, G = grid_for(n);
+    DBuf<long long> cnt(n + 1, s), off(n + 1, s);
+    UA_LAUNCH(k_sq_count, G, 256, 0, s, A, cnt.p);
+    UA_CK(cudaMemsetAsync(cnt.p + n, 0, sizeof(long long), s));
+    exclusive_scan(cnt.p, off.p, n + 1, s);
+    long long total = 0;
+    UA_CK(cudaMemcpyAsync(&total, off.p + n, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    DBuf<unsigned long long> keys(std::max(total, 1ll), s), sorted(std::max(total, 1ll), s), uniq(std::max(total, 1ll), s);
+    UA_LAUNCH(k_sq_expand, G, 256, 0, s, A, off.p, keys.p);
+    size_t tmp = 0;
+    UA_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.p, sorted.p, (int)total, 0, 64, s));
+    DBuf<char> t(tmp, s);
+    UA_CK(cub::DeviceRadixSort::SortKeys(t.p, tmp, keys.p, sorted.p, (int)total, 0, 64, s));
+    DBuf<int> nu(1, s);
+    tmp = 0;
+    UA_CK(cub::DeviceSelect::Unique(nullptr, tmp, sorted.p, uniq.p, nu.p, (int)total, s));
+    DBuf<char> t2(tmp, s);
+    UA_CK(cub::DeviceSelect::Unique(t2.p, tmp, sorted.p, uniq.p, nu.p, (int)total, s));
+    int h_nu = 0;
+    UA_CK(cudaMemcpyAsync(&h_nu, nu.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    squared_pattern_finish(n, uniq.p, h_nu, out_ptr, out_idx, s);
+    return h_nu;
+}
+
+__global__ void k_sq_rows(int n, const unsigned long long* u, int m, int* ptr, int* idx) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
+        const int r = (int)(u[t] >> 32);
+        if (idx) idx[t] = (int)(u[t] & 0xffffffffu);
+        const int rp = t == 0 ? -1 : (int)(u[t - 1] >> 32);
+        for (int q = rp + 1; q <= r; ++q) ptr[q] = t;
+        if (t == m - 1)
+            for (int q = r + 1; q <= n; ++q) ptr[q] = m;
+    }
+}
+void squared_pattern_finish(int n, const unsigned long long* uniq, int m, int* out_ptr, int* out_idx, cudaStream_t s) {
+    if (m == 0) {
+        UA_CK(cudaMemsetAsync(out_ptr, 0, sizeof(int) * (n + 1), s));
+        return;
+    }
+    UA_LAUNCH(k_sq_rows, grid_for(m), 256, 0, s, n, uniq, m, out_ptr, out_idx);
+}
+
+void galerkin_table(const Csr& A, const int* v2a, int nc, int* out_ptr, int* out_col, double* out_val,
+                    long long* nnz_c, cudaStream_t s) {
+    DBuf<int> agg_ptr(nc + 1, s), members(std::max(A.n, 1), s);
+    build_members(A.n, nc, v2a, agg_ptr.p, members.p, s);
+    DBuf<int> rp, ci;
+    DBuf<double> av;
+    long long m = device_galerkin(A, v2a, nc, agg_ptr.p, members.p, rp, ci, av, s);
+    *nnz_c = m;
+    UA_CK(cudaMemcpyAsync(out_ptr, rp.p, sizeof(int) * (nc + 1), cudaMemcpyDeviceToDevice, s));
+    if (out_col && m) {
+        UA_CK(cudaMemcpyAsync(out_col, ci.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, s));
+        UA_CK(cudaMemcpyAsync(out_val, av.p, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    }
+    UA_CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace uaamg

@@ -1,0 +1,742 @@
+// runtime.cu -- device-resident hierarchy, setup driver, K-cycle / NPCG
+// orchestration and the uaamg_* driver ABI.
+//
+// setup    : U/hierarchy.py:120-153 (aggregate -> Galerkin per level, dense
+//            coarsest factorization, complexities)
+// solve    : U/solvers.py:128-255.  One NPCG iteration (the whole K-cycle
+//            recursion, its inner flexible-CG steps, the outer direction /
+//            update) is a fixed kernel sequence; it is captured once into a
+//            CUDA graph per iteration parity (p / p_prev swap roles) and
+//            replayed.  Data-dependent control -- inner-FCG breaks
+//            (U/solvers.py:169,179-180), breakdown, convergence, restarts --
+//            lives in device flags that gate kernels, so the host never waits
+//            on a scalar inside an iteration.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "setup.h"
+
+namespace uaamg {
+
+thread_local std::string g_last_error;
+
+struct Level {
+    int n = 0;
+    long long nnz = 0;
+    DBuf<int> rp, ci;
+    DBuf<double> av;
+    DBuf<int> blk;
+    int nb = 0;
+    int nc = 0;  // 0 on the coarsest level
+    DBuf<int> v2a, seeds, agg_ptr, members, mblk;
+    int mnb = 0;
+    Csr csr() const {
+        Csr c;
+        c.n = n; c.nnz = (int)nnz; c.rp = rp.p; c.ci = ci.p; c.av = av.p;
+        return c;
+    }
+    Blocks blocks() const { return Blocks{nb, blk.p}; }
+    Blocks mblocks() const { return Blocks{mnb, mblk.p}; }
+};
+
+struct LevelWs {
+    DBuf<double> invm, r, rhs, e, tA, tB, bp;                // cycle
+    DBuf<double> xf, rf, z, p0, p1, ap0, ap1;                // inner FCG
+};
+
+struct SolveWs {
+    uaamg_solve_params key{};
+    bool ready = false;
+    std::vector<LevelWs> lev;
+    DBuf<FcgState> fcg;     // one per level
+    DBuf<NpcgState> npcg;
+    DBuf<double> partials;
+    DBuf<unsigned> ticket;
+    DBuf<double> sums;      // per-level scratch sums (singular)
+    DBuf<int> err;          // incompatibility flag
+    DBuf<int> bad_row;
+    // outer vectors
+    DBuf<double> r, z, p0, p1, ap0, ap1, hist, bproj;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    uint64_t graph_kernels[2] = {0, 0};  // kernel launches recorded per graph
+    // level-0 hot-kernel timing (profile_level0): event pairs per graph parity
+    // around the residual, fused up-sweep and direction-SpMV kernels
+    cudaEvent_t pev[2][6] = {};
+    bool profiled = false;
+    double prof_seconds[3] = {0, 0, 0};  // residual, up-sweep, direction SpMV
+    int64_t prof_count = 0;
+    bool graphs_built = false;
+    double* graph_x = nullptr;  // graphs bake in the iterate pointer
+    int* h_flags = nullptr;  // pinned
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~SolveWs() {
+        for (auto& g : graph) if (g) cudaGraphExecDestroy(g);
+        for (auto& row : pev)
+            for (auto& e : row) if (e) cudaEventDestroy(e);
+        if (h_flags) cudaFreeHost(h_flags);
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace uaamg
+
+struct uaamg_hierarchy {
+    std::vector<std::unique_ptr<uaamg::Level>> levels;
+    bool singular = false;
+    int coarse_mode = 0;
+    uaamg::DBuf<double> Minv;
+    double grid_complexity = 1, operator_complexity = 1, setup_seconds = 0;
+    cudaStream_t stream = 0;  // library-owned non-blocking stream (capturable)
+    std::unique_ptr<uaamg::SolveWs> ws;
+    std::mutex mu;
+    ~uaamg_hierarchy() {
+        ws.reset();
+        levels.clear();
+        Minv.release();
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+namespace uaamg {
+
+// ------------------------------------------------------------------ helpers
+// Orders the library's own stream after the caller's stream on entry and the
+// caller's stream after the library's on exit (the caller may pass the legacy
+// default stream, which cannot be graph-captured).
+struct StreamJoin {
+    cudaStream_t caller, own;
+    StreamJoin(cudaStream_t c, cudaStream_t o) : caller(c), own(o) {
+        if (c == o) return;
+        cudaEvent_t ev;
+        UA_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        UA_CK(cudaEventRecord(ev, c));
+        UA_CK(cudaStreamWaitEvent(o, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    ~StreamJoin() {
+        if (caller == own) return;
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;
+        cudaEventRecord(ev, own);
+        cudaStreamWaitEvent(caller, ev, 0);
+        cudaEventDestroy(ev);
+    }
+};
+
+__global__ void k_maxabs_vals(int m, const double* v, unsigned long long* out) {
+    double mx = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) mx = fmax(mx, fabs(v[i]));
+    atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+}
+__global__ void k_fill(int n, double* v, double x) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = x;
+}
+__global__ void k_compose(int n, int* v2a, const int* v2b) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v2a[i] = v2b[v2a[i]];
+}
+__global__ void k_compose_seeds(int nc2, const int* seeds1, const int* sb, int* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc2; i += gridDim.x * blockDim.x) out[i] = seeds1[sb[i]];
+}
+
+static int g1d(long long n) { return std::max(1, std::min(cdiv(n, 256), 4 * kNumSMs)); }
+
+// U/hierarchy.py:112-117
+static bool detect_singular(const Level& L, cudaStream_t s) {
+    if (L.nnz == 0) return true;
+    DBuf<double> ones(L.n, s), y(L.n, s);
+    DBuf<unsigned long long> mx(2, s);
+    UA_CK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
+    UA_LAUNCH(k_fill, g1d(L.n), 256, 0, s, L.n, ones.p, 1.0);
+    launch_spmv(L.csr(), L.blocks(), ones.p, y.p, s);
+    UA_LAUNCH(k_maxabs_vals, g1d(L.nnz), 256, 0, s, (int)L.nnz, L.av.p, mx.p);
+    UA_LAUNCH(k_maxabs_vals, g1d(L.n), 256, 0, s, L.n, y.p, mx.p + 1);
+    unsigned long long h[2];
+    UA_CK(cudaMemcpyAsync(h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    double scale, ax;
+    std::memcpy(&scale, &h[0], 8);
+    std::memcpy(&ax, &h[1], 8);
+    return ax <= 1e-10 * scale;
+}
+
+static void finish_level(Level& L, cudaStream_t s) { build_row_blocks(L.n, L.rp.p, L.blk, L.nb, s); }
+
+// aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)
+static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t s) {
+    DBuf<int> deg(L.n, s);
+    launch_degrees(L.csr(), deg.p, s);
+    L.v2a.alloc(L.n, s);
+    DBuf<int> seeds(L.n, s);
+    int nc = device_aggregate(L.csr(), deg.p, P.seed, P.max_passes, P.size_cap, L.v2a.p, seeds.p, s, nullptr);
+    if (P.passes_per_level == 2) {
+        // aggregate o galerkin o aggregate, composed (U/hierarchy.py:135-138,
+        // U/aggregation.py:206-216)
+        DBuf<int> aptr(nc + 1, s), mem(L.n, s);
+        build_members(L.n, nc, L.v2a.p, aptr.p, mem.p, s);
+        Level M;
+        M.n = nc;
+        M.nnz = device_galerkin(L.csr(), L.v2a.p, nc, aptr.p, mem.p, M.rp, M.ci, M.av, s);
+        DBuf<int> deg2(nc, s), v2b(nc, s), sb(nc, s);
+        launch_degrees(M.csr(), deg2.p, s);
+        int nc2 = device_aggregate(M.csr(), deg2.p, P.seed, P.max_passes, P.size_cap, v2b.p, sb.p, s, nullptr);
+        UA_LAUNCH(k_compose, g1d(L.n), 256, 0, s, L.n, L.v2a.p, v2b.p);
+        DBuf<int> s2(std::max(nc2, 1), s);
+        UA_LAUNCH(k_compose_seeds, g1d(nc2), 256, 0, s, nc2, seeds.p, sb.p, s2.p);
+        UA_CK(cudaStreamSynchronize(s));
+        nc = nc2;
+        seeds = std::move(s2);
+    }
+    L.nc = nc;
+    L.seeds.alloc(std::max(nc, 1), s);
+    UA_CK(cudaMemcpyAsync(L.seeds.p, seeds.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
+}
+
+static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
+                                   const uaamg_setup_params& P, cudaStream_t s) {
+    if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
+    auto h = std::make_unique<uaamg_hierarchy>();
+    UA_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    StreamJoin join(s, h->stream);
+    s = h->stream;
+    cudaEvent_t e0, e1;
+    UA_CK(cudaEventCreate(&e0));
+    UA_CK(cudaEventCreate(&e1));
+    UA_CK(cudaEventRecord(e0, s));
+    auto L0 = std::make_unique<Level>();
+    L0->n = n;
+    L0->nnz = nnz;
+    L0->rp.alloc(n + 1, s);
+    L0->ci.alloc(std::max(nnz, 1ll), s);
+    L0->av.alloc(std::max(nnz, 1ll), s);
+    UA_CK(cudaMemcpyAsync(L0->rp.p, rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+    UA_CK(cudaMemcpyAsync(L0->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+    UA_CK(cudaMemcpyAsync(L0->av.p, av, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    finish_level(*L0, s);
+    h->singular = P.singular < 0 ? detect_singular(*L0, s) : (P.singular != 0);
+    const int max_levels = P.max_levels;
+    std::unique_ptr<Level> cur = std::move(L0);
+    while (cur->n > P.n0 && (int)h->levels.size() < max_levels - 1) {
+        aggregate_level(*cur, P, s);
+        if (cur->nc == cur->n)
+            throw Error(UAAMG_ESETUP, "aggregation stagnated at level " + std::to_string(h->levels.size()) + ": " +
+                                          std::to_string(cur->n) + " vertices produced no coarsening");
+        cur->agg_ptr.alloc(cur->nc + 1, s);
+        cur->members.alloc(cur->n, s);
+        build_members(cur->n, cur->nc, cur->v2a.p, cur->agg_ptr.p, cur->members.p, s);
+        build_row_blocks(cur->nc, cur->agg_ptr.p, cur->mblk, cur->mnb, s);
+        auto nxt = std::make_unique<Level>();
+        nxt->n = cur->nc;
+        nxt->nnz = device_galerkin(cur->csr(), cur->v2a.p, cur->nc, cur->agg_ptr.p, cur->members.p, nxt->rp, nxt->ci,
+                                   nxt->av, s);
+        finish_level(*nxt, s);
+        h->levels.push_back(std::move(cur));
+        cur = std::move(nxt);
+    }
+    h->levels.push_back(std::move(cur));
+    h->coarse_mode = device_coarse_factor(h->levels.back()->csr(), h->singular, h->Minv, s);
+    UA_CK(cudaEventRecord(e1, s));
+    UA_CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    UA_CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->setup_seconds = ms * 1e-3;
+    double sn = 0, snz = 0;
+    for (auto& L : h->levels) { sn += L->n; snz += (double)L->nnz; }
+    h->grid_complexity = sn / h->levels[0]->n;
+    h->operator_complexity = snz / std::max<double>((double)h->levels[0]->nnz, 1.0);
+    return h.release();
+}
+
+// ------------------------------------------------------------------ solve plan
+struct Plan {
+    uaamg_hierarchy* h;
+    SolveWs* ws;
+    uaamg_solve_params p;
+    cudaStream_t s;
+    int prof = -1;  // >= 0: record level-0 timing events of this parity
+    void mark(int k) {
+        if (prof >= 0) UA_CK(cudaEventRecord(ws->pev[prof][k], s));
+    }
+    RedScratch rs() const { return RedScratch{ws->partials.p, ws->ticket.p}; }
+    int coarsest() const { return (int)h->levels.size() - 1; }
+    bool sing() const { return h->singular; }
+
+    // U/solvers.py:128-157
+    void cycle(int l, const double* b, double* out, const int* gate) {
+        Level& L = *h->levels[l];
+        LevelWs& W = ws->lev[l];
+        if (sing()) {
+            launch_check_compatible(L.n, b, W.bp.p, ws->err.p, ws->sums.p + 4 * l, gate, l, rs(), s);
+            b = W.bp.p;
+        }
+        if (l == coarsest()) {
+            launch_dense_solve(L.n, h->Minv.p, b, out, gate, s);
+            if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 2, gate, rs(), s);
+            return;
+        }
+        const Csr A = L.csr();
+        const Blocks B = L.blocks();
+        // pre-smoothing from a zero guess
+        int xmode = p.pre_sweeps == 0 ? 0 : (p.pre_sweeps == 1 ? 1 : 2);
+        const double* xpre = nullptr;
+        double* cur = W.tA.p;
+        if (xmode == 2) {
+            launch_xpre1(L.n, W.invm.p, b, W.tA.p, gate, s);
+            for (int k = 1; k < p.pre_sweeps; ++k) {
+                double* nx = (cur == W.tA.p) ? W.tB.p : W.tA.p;
+                launch_sweep_vec(A, B, W.invm.p, b, cur, nx, gate, s);
+                cur = nx;
+            }
+            xpre = cur;
+        }
+        // r = b - A x ; r_c = restrict(r)
+        if (l == 0) mark(0);
+        launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, s);
+        if (l == 0) mark(1);
+        LevelWs& C = ws->lev[l + 1];
+        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mblocks(), W.r.p, C.rhs.p, gate, s);
+        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), s);
+        const bool exact = (l + 1 == coarsest());
+        const double* ec;
+        const int* ec_valid = nullptr;
+        if (!p.kcycle || p.inner_krylov_steps == 0 || exact) {
+            cycle(l + 1, C.rhs.p, C.e.p, gate);
+            ec = C.e.p;
+        } else {
+            fcg(l + 1, C.rhs.p, C.xf.p, gate);
+            ec = C.xf.p;
+            ec_valid = &ws->fcg.p[l + 1].upd[0];
+        }
+        // prolongate + post-smoothing
+        if (p.post_sweeps == 0) {
+            launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, s);
+        } else {
+            double* other = (xpre == W.tA.p) ? W.tB.p : W.tA.p;
+            double* dst = p.post_sweeps == 1 ? out : other;
+            if (l == 0) mark(2);
+            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, s);
+            if (l == 0) mark(3);
+            double* c2 = dst;
+            for (int k = 1; k < p.post_sweeps; ++k) {
+                double* nx = (k == p.post_sweeps - 1) ? out : ((c2 == W.tA.p) ? W.tB.p : W.tA.p);
+                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, s);
+                c2 = nx;
+            }
+        }
+        if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), s);
+    }
+
+    // U/solvers.py:160-187
+    void fcg(int l, const double* b, double* x, const int* parent_gate) {
+        Level& L = *h->levels[l];
+        LevelWs& W = ws->lev[l];
+        FcgState* st = ws->fcg.p + l;
+        launch_fcg_begin(L.n, b, parent_gate, st, rs(), s);
+        double* P[2] = {W.p0.p, W.p1.p};
+        double* AP[2] = {W.ap0.p, W.ap1.p};
+        for (int k = 0; k < p.inner_krylov_steps; ++k) {
+            const int* g = &st->gate[k];
+            const double* rin = (k == 0) ? b : W.rf.p;
+            cycle(l, rin, W.z.p, g);
+            double* pc = P[k & 1];
+            double* pp = P[(k + 1) & 1];
+            double* apc = AP[k & 1];
+            double* app = AP[(k + 1) & 1];
+            if (k > 0) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), s);
+            launch_dir_fcg(L.csr(), L.blocks(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), s);
+            launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), s);
+        }
+    }
+
+    // one NPCG iteration (U/solvers.py:221-254); parity selects p/p_prev roles
+    void npcg_iteration(double* x, int parity) {
+        Level& L = *h->levels[0];
+        NpcgState* st = ws->npcg.p;
+        const int* act = &st->active;
+        double* P[2] = {ws->p0.p, ws->p1.p};
+        double* AP[2] = {ws->ap0.p, ws->ap1.p};
+        double* pc = P[parity];
+        double* pp = P[parity ^ 1];
+        double* apc = AP[parity];
+        double* app = AP[parity ^ 1];
+        cycle(0, ws->r.p, ws->z.p, act);
+        if (sing()) launch_project_mean(L.n, ws->z.p, &st->sum, act, rs(), s);
+        launch_beta(L.n, ws->z.p, pp, app, &st->beta, act, &st->have_prev, rs(), s);
+        mark(4);
+        launch_dir_npcg(L.csr(), L.blocks(), ws->z.p, pp, ws->r.p, pc, apc, st, rs(), s);
+        mark(5);
+        launch_npcg_update(L.n, x, pc, ws->r.p, apc, st, ws->hist.p, sing(), rs(), s);
+    }
+};
+
+static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s) {
+    auto& ws = h->ws;
+    const bool same = ws && ws->ready && ws->key.kcycle == p.kcycle &&
+                      ws->key.inner_krylov_steps == p.inner_krylov_steps && ws->key.pre_sweeps == p.pre_sweeps &&
+                      ws->key.post_sweeps == p.post_sweeps && ws->key.smoother_l1 == p.smoother_l1 &&
+                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters;
+    if (same) return;
+    if (ws) UA_CK(cudaStreamSynchronize(s));
+    ws.reset(new SolveWs());
+    ws->key = p;
+    const int nl = (int)h->levels.size();
+    ws->lev.resize(nl);
+    ws->fcg.alloc(nl, s);
+    UA_CK(cudaMemsetAsync(ws->fcg.p, 0, sizeof(FcgState) * nl, s));
+    ws->npcg.alloc(1, s);
+    UA_CK(cudaMemsetAsync(ws->npcg.p, 0, sizeof(NpcgState), s));
+    ws->partials.alloc(4 * (size_t)kMaxRedBlocks, s);
+    ws->ticket.alloc(1, s);
+    UA_CK(cudaMemsetAsync(ws->ticket.p, 0, sizeof(unsigned), s));
+    ws->sums.alloc(4 * nl + 4, s);
+    ws->err.alloc(1, s);
+    UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
+    ws->bad_row.alloc(1, s);
+    const bool sing = h->singular;
+    for (int l = 0; l < nl; ++l) {
+        Level& L = *h->levels[l];
+        LevelWs& W = ws->lev[l];
+        const size_t n = std::max(L.n, 1);
+        if (sing) W.bp.alloc(n, s);
+        if (l > 0) { W.rhs.alloc(n, s); W.e.alloc(n, s); }
+        if (l == nl - 1) continue;
+        W.invm.alloc(n, s);
+        W.r.alloc(n, s);
+        W.tA.alloc(n, s);
+        W.tB.alloc(n, s);
+        if (l > 0 && p.kcycle && p.inner_krylov_steps > 0) {
+            W.xf.alloc(n, s); W.rf.alloc(n, s); W.z.alloc(n, s);
+            W.p0.alloc(n, s); W.p1.alloc(n, s); W.ap0.alloc(n, s); W.ap1.alloc(n, s);
+        }
+        // smoother diagonal, hoisted out of the cycle (the reference
+        // recomputes it per smooth() call with identical values)
+        int h_bad = 0x7fffffff;
+        UA_CK(cudaMemcpyAsync(ws->bad_row.p, &h_bad, sizeof(int), cudaMemcpyHostToDevice, s));
+        launch_inv_diag(L.csr(), p.smoother_l1, p.omega, W.invm.p, ws->bad_row.p, s);
+        UA_CK(cudaMemcpyAsync(&h_bad, ws->bad_row.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        if (h_bad != 0x7fffffff) {
+            ws.reset();
+            throw Error(UAAMG_ENUMERICAL, "non-positive smoother diagonal at row " + std::to_string(h_bad));
+        }
+    }
+    const size_t n0 = h->levels[0]->n;
+    ws->r.alloc(n0, s); ws->z.alloc(n0, s); ws->p0.alloc(n0, s); ws->p1.alloc(n0, s);
+    ws->ap0.alloc(n0, s); ws->ap1.alloc(n0, s); ws->bproj.alloc(n0, s);
+    ws->hist.alloc((size_t)p.max_iters + 1, s);
+    UA_CK(cudaMallocHost(&ws->h_flags, 4 * sizeof(int)));
+    UA_CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
+    UA_CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
+    if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
+    ws->ready = true;
+    UA_CK(cudaStreamSynchronize(s));
+}
+
+static void build_graphs(Plan& pl, double* x) {
+    SolveWs* ws = pl.ws;
+    if (pl.p.profile_level0 && !ws->pev[0][0])
+        for (auto& row : ws->pev)
+            for (auto& e : row) UA_CK(cudaEventCreate(&e));
+    ws->profiled = pl.p.profile_level0 != 0;
+    for (int par = 0; par < 2; ++par) {
+        cudaGraph_t g;
+        const uint64_t before = g_launches.load();
+        UA_CK(cudaStreamBeginCapture(pl.s, cudaStreamCaptureModeThreadLocal));
+        pl.prof = pl.p.profile_level0 ? par : -1;
+        pl.npcg_iteration(x, par);
+        pl.prof = -1;
+        UA_CK(cudaStreamEndCapture(pl.s, &g));
+        // captured launches are not executions: account them per replay
+        ws->graph_kernels[par] = g_launches.load() - before;
+        g_launches.fetch_sub(ws->graph_kernels[par]);
+        if (ws->graph[par]) cudaGraphExecDestroy(ws->graph[par]);
+        UA_CK(cudaGraphInstantiate(&ws->graph[par], g, 0));
+        cudaGraphDestroy(g);
+    }
+    ws->graphs_built = true;
+}
+
+__global__ void k_set_npcg(NpcgState* st, double tol, int max_iters) {
+    st->tol = tol;
+    st->max_iters = max_iters;
+}
+
+static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const double* b, const double* x0, double* x,
+                     double* hist_host, uaamg_solve_result* res, cudaStream_t s) {
+    if (!(p.tol > 0)) throw Error(UAAMG_EINVAL, "tol must be positive");
+    std::lock_guard<std::mutex> lk(h->mu);
+    StreamJoin join(s, h->stream);
+    s = h->stream;
+    ensure_ws(h, p, s);
+    SolveWs* ws = h->ws.get();
+    Plan pl{h, ws, p, s};
+    Level& L = *h->levels[0];
+    const int n = L.n;
+    cudaEvent_t e0, e1;
+    UA_CK(cudaEventCreate(&e0));
+    UA_CK(cudaEventCreate(&e1));
+    UA_CK(cudaEventRecord(e0, s));
+    const double* bb = b;
+    if (h->singular) {
+        // U/solvers.py:203-204
+        UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
+        launch_check_compatible(n, b, ws->bproj.p, ws->err.p, ws->sums.p + 4 * (int)h->levels.size(), nullptr, -1,
+                                pl.rs(), s);
+        int herr = 0;
+        UA_CK(cudaMemcpyAsync(&herr, ws->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        if (herr) {
+            res->iterations = 0;
+            res->converged = 0;
+            throw Error(UAAMG_ENUMERICAL, "right-hand side at the finest level has a null-space component");
+        }
+        bb = ws->bproj.p;
+    }
+    // x, r initial (U/solvers.py:208-215)
+    if (x0) {
+        UA_CK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        if (h->singular) launch_project_mean(n, x, ws->sums.p, nullptr, pl.rs(), s);
+        launch_spmv(L.csr(), L.blocks(), x, ws->z.p, s);
+        launch_axpby_init(n, bb, ws->z.p, ws->r.p, s);
+    } else {
+        UA_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+        launch_copy(n, bb, ws->r.p, s);
+    }
+    UA_LAUNCH(k_set_npcg, 1, 1, 0, s, ws->npcg.p, p.tol, p.max_iters);
+    launch_npcg_init(n, bb, ws->r.p, ws->npcg.p, ws->hist.p, pl.rs(), s);
+    UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
+    // iterations: pipelined launches, at most one no-op iteration past the end
+    NpcgState hst{};
+    UA_CK(cudaMemcpyAsync(&hst, ws->npcg.p, sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    if (hst.bnorm == 0.0) UA_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));  // U/solvers.py:206-207
+    if (p.use_graphs && (!ws->graphs_built || ws->graph_x != x || ws->profiled != (p.profile_level0 != 0))) {
+        build_graphs(pl, x);
+        ws->graph_x = x;
+    }
+    int launched = 0;
+    int64_t prof_n = 0;
+    double prof_s[3] = {0, 0, 0};
+    const bool prof = p.use_graphs && p.profile_level0;
+    auto harvest = [&](int par) {
+        // level-0 kernel durations of the replay that just completed
+        for (int k = 0; k < 3; ++k) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, ws->pev[par][2 * k], ws->pev[par][2 * k + 1]) == cudaSuccess)
+                prof_s[k] += t * 1e-3;
+        }
+        ++prof_n;
+    };
+    if (hst.active) {
+        // Pipelined: iteration it is launched before iteration it-1's
+        // "active" flag is read, so at most one gated no-op replay runs past
+        // convergence.  `before[par]`: was the solve active when the replay of
+        // that parity started (only such replays are harvested for timing).
+        int before[2] = {1, 0};
+        int last_par = -1;
+        for (int it = 0; it < p.max_iters; ++it) {
+            const int par = it & 1;
+            if (p.use_graphs) {
+                UA_CK(cudaGraphLaunch(ws->graph[par], s));
+                g_launches.fetch_add(ws->graph_kernels[par]);
+            } else {
+                pl.npcg_iteration(x, par);
+            }
+            ++launched;
+            last_par = par;
+            UA_CK(cudaMemcpyAsync(ws->h_flags + par, &ws->npcg.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+            UA_CK(cudaEventRecord(ws->ev[par], s));
+            if (it >= 1) {
+                UA_CK(cudaEventSynchronize(ws->ev[par ^ 1]));
+                if (prof && before[par ^ 1]) harvest(par ^ 1);
+                before[par] = ws->h_flags[par ^ 1];
+                before[par ^ 1] = 0;
+                if (ws->h_flags[par ^ 1] == 0) { last_par = -1; break; }
+            }
+        }
+        if (last_par >= 0) {
+            UA_CK(cudaEventSynchronize(ws->ev[last_par]));
+            if (prof && before[last_par]) harvest(last_par);
+        }
+    }
+    UA_CK(cudaEventRecord(e1, s));
+    UA_CK(cudaMemcpyAsync(&hst, ws->npcg.p, sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+    int herr = 0;
+    UA_CK(cudaMemcpyAsync(&herr, ws->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    float ms = 0;
+    UA_CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    res->iterations = hst.iters;
+    res->solve_seconds = ms * 1e-3;
+    res->l0_kernel_launches = prof_n;
+    res->l0_kernel_seconds = prof_s[1];
+    res->l0_kernel_bytes = 0;
+    (void)launched;
+    ws->prof_seconds[0] = prof_s[0];
+    ws->prof_seconds[1] = prof_s[1];
+    ws->prof_seconds[2] = prof_s[2];
+    ws->prof_count = prof_n;
+    const int nh = hst.iters + 1;
+    if (hist_host) UA_CK(cudaMemcpy(hist_host, ws->hist.p, sizeof(double) * nh, cudaMemcpyDeviceToHost));
+    res->converged = (hst.bnorm == 0.0) ? 1 : (hst.last_rel <= p.tol);
+    res->status = 0;
+    if (herr) {
+        res->converged = 0;
+        res->status = UAAMG_ENUMERICAL;
+        throw Error(UAAMG_ENUMERICAL, "right-hand side at a coarse level has a null-space component (relative size > 1e-10)");
+    }
+    if (hst.status == 1) {
+        res->converged = 0;
+        res->status = UAAMG_ENUMERICAL;
+        char buf[160];
+        snprintf(buf, sizeof buf, "conjugate-gradient breakdown at iteration %d: p'Ap = %.3e", hst.iters + 1, hst.pap);
+        throw Error(UAAMG_ENUMERICAL, buf);
+    }
+    return 0;
+}
+
+}  // namespace uaamg
+
+// ====================================================================== C ABI
+using namespace uaamg;
+
+#define UA_GUARD(...)                                           \
+    try {                                                       \
+        __VA_ARGS__;                                                 \
+        return UAAMG_OK;                                        \
+    } catch (const Error& e) {                                  \
+        g_last_error = e.what();                                \
+        return e.code;                                          \
+    } catch (const std::exception& e) {                         \
+        g_last_error = e.what();                                \
+        return UAAMG_ECUDA;                                     \
+    }
+
+extern "C" {
+
+int uaamg_version(void) { return 1; }
+const char* uaamg_last_error(void) { return g_last_error.c_str(); }
+uint64_t uaamg_launch_count(void) { return g_launches.load(); }
+
+int uaamg_setup(int n, int64_t nnz, const int* row_ptr, const int* col, const double* val,
+                const uaamg_setup_params* params, uaamg_hierarchy** out, void* stream) {
+    UA_GUARD({
+        if (!params || !out) throw Error(UAAMG_EINVAL, "null argument");
+        if (params->passes_per_level != 1 && params->passes_per_level != 2)
+            throw Error(UAAMG_EAGG, "passes_per_level must be 1 or 2");
+        if (params->max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
+        *out = setup_impl(n, nnz, row_ptr, col, val, *params, (cudaStream_t)stream);
+    })
+}
+
+void uaamg_hierarchy_free(uaamg_hierarchy* h) {
+    if (!h) return;
+    delete h;
+}
+
+int uaamg_hierarchy_get_info(const uaamg_hierarchy* h, uaamg_hierarchy_info* info) {
+    UA_GUARD({
+        info->n_levels = (int)h->levels.size();
+        info->singular = h->singular;
+        info->grid_complexity = h->grid_complexity;
+        info->operator_complexity = h->operator_complexity;
+        info->setup_seconds = h->setup_seconds;
+    })
+}
+
+int uaamg_hierarchy_level(const uaamg_hierarchy* h, int level, uaamg_level_view* v) {
+    UA_GUARD({
+        if (level < 0 || level >= (int)h->levels.size()) throw Error(UAAMG_EINVAL, "level out of range");
+        const Level& L = *h->levels[level];
+        v->n = L.n;
+        v->nnz = L.nnz;
+        v->row_ptr = L.rp.p;
+        v->col = L.ci.p;
+        v->val = L.av.p;
+        v->n_coarse = L.nc;
+        v->vertex_to_agg = L.nc ? L.v2a.p : nullptr;
+        v->coarse_vertex_of_agg = L.nc ? L.seeds.p : nullptr;
+        v->agg_ptr = L.nc ? L.agg_ptr.p : nullptr;
+        v->members = L.nc ? L.members.p : nullptr;
+    })
+}
+
+int uaamg_npcg_solve(uaamg_hierarchy* h, const uaamg_solve_params* p, const double* b, const double* x0, double* x,
+                     double* history_host, uaamg_solve_result* res, void* stream) {
+    UA_GUARD({
+        std::memset(res, 0, sizeof(*res));
+        npcg_impl(h, *p, b, x0, x, history_host, res, (cudaStream_t)stream);
+    })
+}
+
+int uaamg_solve_profile(const uaamg_hierarchy* h, double* seconds3, double* bytes3, int64_t* count) {
+    UA_GUARD({
+        if (!h->ws) throw Error(UAAMG_EINVAL, "no solve has run on this hierarchy");
+        const Level& L = *h->levels[0];
+        const double n = L.n, nnz = (double)L.nnz, nc = L.nc;
+        const double csr = 12.0 * nnz + 4.0 * (n + 1);
+        // algorithmic bytes per launch ("Roofline"); x of the
+        // one-sweep pre-smoother is rebuilt from b and inv_m on the fly
+        bytes3[0] = csr + 24.0 * n;             // residual: b, inv_m in; r out
+        bytes3[1] = csr + 28.0 * n + 8.0 * nc;  // up-sweep: b, inv_m, v2a, e_c in; x out
+        bytes3[2] = csr + 40.0 * n;             // direction SpMV: z, p_prev, r in; p, Ap out
+        for (int k = 0; k < 3; ++k) seconds3[k] = h->ws->prof_seconds[k];
+        *count = h->ws->prof_count;
+    })
+}
+
+int uaamg_cycle(uaamg_hierarchy* h, const uaamg_solve_params* p, int level, const double* b, double* x,
+                void* stream) {
+    UA_GUARD({
+        if (level < 0 || level >= (int)h->levels.size()) throw Error(UAAMG_EINVAL, "level out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        StreamJoin join((cudaStream_t)stream, h->stream);
+        cudaStream_t s = h->stream;
+        ensure_ws(h, *p, s);
+        Plan pl{h, h->ws.get(), *p, s};
+        UA_CK(cudaMemsetAsync(h->ws->err.p, 0, sizeof(int), s));
+        pl.cycle(level, b, x, nullptr);
+        int herr = 0;
+        UA_CK(cudaMemcpyAsync(&herr, h->ws->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        if (herr) throw Error(UAAMG_ENUMERICAL, "right-hand side has a null-space component (relative size > 1e-10)");
+    })
+}
+
+int uaamg_smooth(uaamg_hierarchy* h, const uaamg_solve_params* p, int level, const double* x, const double* b,
+                 int sweeps, double* out, void* stream) {
+    UA_GUARD({
+        if (level < 0 || level >= (int)h->levels.size() - 1) throw Error(UAAMG_EINVAL, "level out of range");
+        std::lock_guard<std::mutex> lk(h->mu);
+        StreamJoin join((cudaStream_t)stream, h->stream);
+        cudaStream_t s = h->stream;
+        ensure_ws(h, *p, s);
+        Level& L = *h->levels[level];
+        LevelWs& W = h->ws->lev[level];
+        if (sweeps <= 0) {
+            UA_CK(cudaMemcpyAsync(out, x, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, s));
+        } else {
+            const double* cur = x;
+            for (int k = 0; k < sweeps; ++k) {
+                double* nx = (k == sweeps - 1) ? out : ((cur == W.tA.p) ? W.tB.p : W.tA.p);
+                launch_sweep_vec(L.csr(), L.blocks(), W.invm.p, b, cur, nx, nullptr, s);
+                cur = nx;
+            }
+        }
+        UA_CK(cudaStreamSynchronize(s));
+    })
+}
+
+}  // extern "C"

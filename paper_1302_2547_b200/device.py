@@ -1,0 +1,117 @@
+"""Device-side plumbing: torch owns user-visible device memory and streams;
+the CUDA work happens in libuaamg_b200.so.
+
+``DeviceCSR`` is the device twin of :class:`~.sparse.SparseMatrix` (int32
+row_ptr/col, fp64 val -- SURVEY.md section 8 layout).  Library-owned arrays
+(the hierarchy) are exposed to torch zero-copy through
+``__cuda_array_interface__`` views that keep their owner alive.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_TYPESTR = {np.dtype(np.int32): "<i4", np.dtype(np.float64): "<f8", np.dtype(np.uint8): "|u1",
+            np.dtype(np.int64): "<i8"}
+_TORCH = {np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
+          np.dtype(np.int64): torch.int64}
+
+
+def cuda_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 UA-AMG path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    """Current torch CUDA stream handle (passed to every library call)."""
+    return ctypes_stream(torch.cuda.current_stream())
+
+
+def ctypes_stream(s):
+    return s.cuda_stream
+
+
+def to_device(a, dtype):
+    """numpy / torch -> contiguous device tensor of ``dtype`` (numpy dtype)."""
+    dt = _TORCH[np.dtype(dtype)]
+    if isinstance(a, torch.Tensor):
+        return a.to(device=cuda_device(), dtype=dt).contiguous()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return torch.from_numpy(arr).to(device=cuda_device(), non_blocking=False)
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+class _CudaView:
+    """Minimal __cuda_array_interface__ exporter for library-owned memory."""
+
+    def __init__(self, address, n, dtype, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": _TYPESTR[np.dtype(dtype)], "data": (int(address or 0), True),
+            "version": 2, "strides": None,
+        }
+
+
+def view(address, n, dtype, owner):
+    """Zero-copy torch view of ``n`` elements at a library device address."""
+    if n == 0 or not address:
+        return torch.empty(0, dtype=_TORCH[np.dtype(dtype)], device=cuda_device())
+    return torch.as_tensor(_CudaView(address, n, dtype, owner), device=cuda_device())
+
+
+class DeviceCSR:
+    """Device CSR matrix: int32 row_ptr/col, float64 val (square)."""
+
+    __slots__ = ("n_rows", "n_cols", "row_ptr", "col", "val")
+
+    def __init__(self, n_rows, n_cols, row_ptr, col, val):
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.row_ptr, self.col, self.val = row_ptr, col, val
+
+    @classmethod
+    def from_host(cls, a):
+        if a.nnz >= 2 ** 31 or a.n_rows >= 2 ** 31:
+            raise ValueError("matrix too large for int32 device indices")
+        return cls(a.n_rows, a.n_cols, to_device(a.indptr, np.int32), to_device(a.indices, np.int32),
+                   to_device(a.data, np.float64))
+
+    @classmethod
+    def from_arrays(cls, n, row_ptr, col, val):
+        return cls(n, n, to_device(row_ptr, np.int32), to_device(col, np.int32), to_device(val, np.float64))
+
+    @property
+    def nnz(self):
+        return int(self.col.shape[0])
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    def to_host(self):
+        from .sparse import SparseMatrix
+        return SparseMatrix(self.n_rows, self.n_cols, to_host(self.row_ptr).astype(np.int64),
+                            to_host(self.col).astype(np.int64), to_host(self.val), _validate=False)
+
+    def spmv(self, x):
+        """y = A x (bit-identical to the reference's sequential row sums)."""
+        host = not isinstance(x, torch.Tensor)
+        xd = to_device(x, np.float64)
+        if xd.shape != (self.n_cols,):
+            raise ValueError(f"spmv dimension mismatch: matrix {self.shape}, vector {tuple(xd.shape)}")
+        y = torch.empty(self.n_rows, dtype=torch.float64, device=xd.device)
+        _lib.check(_lib.load().uaamg_k_spmv(self.n_rows, ptr(self.row_ptr), ptr(self.col), ptr(self.val),
+                                            ptr(xd), ptr(y), stream()))
+        return to_host(y) if host else y
+
+    def __repr__(self):
+        return f"DeviceCSR(shape={self.shape}, nnz={self.nnz})"

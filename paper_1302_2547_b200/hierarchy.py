@@ -1,0 +1,189 @@
+"""Multilevel hierarchy on the GPU.
+
+Mirrors /root/reference/pkg/src/uaamg/hierarchy.py: ``galerkin_coarse``
+(:22-28), ``CoarseSolver`` (:31-65), ``Level``/``Hierarchy`` (:68-109),
+``detect_singular`` (:112-117), ``setup`` (:120-153).  ``setup`` runs
+entirely on the device (``uaamg_setup``): per level the multi-pass
+aggregation, members_csr, and the Galerkin operator A_c = P^T A P as an
+exact-order segmented sum by aggregate pair; the coarsest level is factored
+densely on the device.  The hierarchy stays device-resident; host mirrors of
+level matrices/aggregations are materialised lazily on attribute access.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .aggregation import Aggregation, AggregationConfig
+from .device import DeviceCSR, ptr, stream, view
+from .sparse import SparseMatrix
+
+
+class SetupError(RuntimeError):
+    pass
+
+
+def galerkin_coarse(a, agg):
+    """(A_c)_IJ = sum over s in G_I, t in G_J of a_st; exact zeros dropped."""
+    if agg.n_fine != a.n_rows or a.n_rows != a.n_cols:
+        raise ValueError("aggregation does not match matrix dimensions")
+    from . import kernel_table
+    p, i, v = kernel_table.galerkin_coo(a.indptr, a.indices, a.data, agg.vertex_to_agg, agg.n_coarse)
+    return SparseMatrix(agg.n_coarse, agg.n_coarse, p, i, v, _validate=False)
+
+
+class _LazyMatrix:
+    """Host SparseMatrix of a device level, materialised on first use."""
+
+
+class Level:
+    """One hierarchy level: ``matrix`` (host SparseMatrix, lazy) and
+    ``aggregation`` (None on the coarsest level); ``device_matrix`` is the
+    zero-copy device CSR."""
+
+    __slots__ = ("_h", "_l", "_matrix", "_agg", "_dev")
+
+    def __init__(self, h, l):
+        self._h, self._l = h, l
+        self._matrix = self._agg = self._dev = None
+
+    def _view(self):
+        return self._h._level_view(self._l)
+
+    @property
+    def device_matrix(self):
+        if self._dev is None:
+            v = self._view()
+            self._dev = DeviceCSR(v.n, v.n, view(v.row_ptr, v.n + 1, np.int32, self._h),
+                                  view(v.col, v.nnz, np.int32, self._h), view(v.val, v.nnz, np.float64, self._h))
+        return self._dev
+
+    @property
+    def matrix(self):
+        if self._matrix is None:
+            self._matrix = self.device_matrix.to_host()
+        return self._matrix
+
+    @property
+    def aggregation(self):
+        if self._agg is None:
+            v = self._view()
+            if v.n_coarse == 0:
+                return None
+            self._agg = Aggregation(v.n, device_arrays=(view(v.vertex_to_agg, v.n, np.int32, self._h),
+                                                        view(v.coarse_vertex_of_agg, v.n_coarse, np.int32, self._h)))
+        return self._agg
+
+    @property
+    def n(self):
+        return self._view().n
+
+    @property
+    def nnz(self):
+        return int(self._view().nnz)
+
+
+class CoarseSolver:
+    """Dense factorization of the coarsest operator, held on the device
+    (Cholesky-based inverse, or eigen pseudo-inverse when singular)."""
+
+    def __init__(self, h):
+        self._h = h
+        self.n = h.levels[-1].n
+        self.singular = h.singular
+
+    def solve(self, b):
+        from .solvers import CycleSpec, Smoother, cycle
+        return cycle(self._h, CycleSpec(), Smoother(), self._h.n_levels - 1, b)
+
+
+class Hierarchy:
+    """Device-resident multilevel hierarchy (reference hierarchy.py:74-109)."""
+
+    def __init__(self, handle, offset=0, parent=None):
+        self._handle = handle
+        self._offset = offset
+        self._parent = parent
+        L = _lib.load()
+        info = _lib.HierarchyInfo()
+        _lib.check(L.uaamg_hierarchy_get_info(handle, ctypes.byref(info)))
+        self._info = info
+        self.singular = bool(info.singular)
+        nl = info.n_levels - offset
+        self.levels = [Level(self, offset + l) for l in range(nl)]
+        n0 = self.levels[0].n
+        nnz0 = max(self.levels[0].nnz, 1)
+        self.grid_complexity = sum(l.n for l in self.levels) / n0
+        self.operator_complexity = sum(l.nnz for l in self.levels) / nnz0
+        self.setup_seconds = float(info.setup_seconds)
+        self.coarsest_solver = CoarseSolver(self)
+
+    def _level_view(self, l):
+        v = _lib.LevelView()
+        _lib.check(_lib.load().uaamg_hierarchy_level(self._handle, l, ctypes.byref(v)))
+        return v
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+    def matrix(self, level):
+        return self.levels[level].matrix
+
+    def sub(self, level):
+        """View of the hierarchy starting at ``level``."""
+        if level == 0:
+            return self
+        return Hierarchy(self._handle, self._offset + level, parent=self)
+
+    def summary(self):
+        rows = []
+        for l, lev in enumerate(self.levels):
+            row = {"level": l, "n": lev.n, "nnz": lev.nnz}
+            agg = lev.aggregation
+            if agg is not None:
+                row["coarsening_ratio"] = agg.coarsening_ratio
+            rows.append(row)
+        return {"levels": rows, "grid_complexity": self.grid_complexity,
+                "operator_complexity": self.operator_complexity, "singular": self.singular}
+
+    def __del__(self):
+        if getattr(self, "_parent", None) is None and getattr(self, "_handle", None):
+            try:
+                _lib.load().uaamg_hierarchy_free(self._handle)
+            except Exception:
+                pass
+            self._handle = None
+
+    def __repr__(self):
+        return f"Hierarchy(levels={[l.n for l in self.levels]})"
+
+
+def detect_singular(a):
+    """A annihilates the constant vector (reference hierarchy.py:112-117)."""
+    if a.nnz == 0:
+        return True
+    scale = np.max(np.abs(a.data))
+    return np.max(np.abs(a.spmv(np.ones(a.n_rows)))) <= 1e-10 * scale
+
+
+def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0, singular=None,
+          reshape_pair_cap=16):
+    """Build the hierarchy on the GPU (reference hierarchy.py:120-153).
+
+    ``a``: host SparseMatrix (uploaded once) or DeviceCSR (used in place)."""
+    if a.n_rows != a.n_cols:
+        raise SetupError("matrix must be square")
+    if reshape_sweeps > 0:
+        raise NotImplementedError("subgraph reshaping (reshape_sweeps > 0) is outside the B200 hot path "
+                                  "(SURVEY.md section 8f, rank 4)")
+    d = a if isinstance(a, DeviceCSR) else a.device()
+    P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
+                         max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
+                         n0=int(n0), max_levels=int(max_levels),
+                         singular=-1 if singular is None else int(bool(singular)))
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
+                                       ctypes.byref(h), stream()))
+    return Hierarchy(h)
