@@ -39,6 +39,8 @@ def to_device(a, dtype):
     if isinstance(a, torch.Tensor):
         return a.to(device=cuda_device(), dtype=dt).contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype)
+    if not arr.flags.writeable:  # SparseMatrix arrays are read-only views
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device=cuda_device(), non_blocking=False)
 
 
@@ -56,7 +58,7 @@ class _CudaView:
     def __init__(self, address, n, dtype, owner):
         self._owner = owner
         self.__cuda_array_interface__ = {
-            "shape": (int(n),), "typestr": _TYPESTR[np.dtype(dtype)], "data": (int(address or 0), True),
+            "shape": (int(n),), "typestr": _TYPESTR[np.dtype(dtype)], "data": (int(address or 0), False),
             "version": 2, "strides": None,
         }
 
