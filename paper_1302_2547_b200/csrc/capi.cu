@@ -143,7 +143,7 @@ int uaamg_k_restrict(int nc, const int* agg_ptr, const int* members, const doubl
     UA_GUARD({
         cudaStream_t s = (cudaStream_t)stream;
         RowBlocksTmp B(nc, agg_ptr, s);
-        launch_restrict(nc, agg_ptr, members, B.get(), r, out, nullptr, s);
+        launch_restrict_exact(nc, agg_ptr, members, B.get(), r, out, s);
     })
 }
 
@@ -166,7 +166,7 @@ int uaamg_k_smooth_sweeps(int n, const int* row_ptr, const int* col, const doubl
             const double* cur = x;
             for (int k = 0; k < sweeps; ++k) {
                 double* nx = (k == sweeps - 1) ? out : ((cur == t0.p) ? t1.p : t0.p);
-                launch_sweep_vec(A, B.get(), inv_m, b, cur, nx, nullptr, s);
+                launch_sweep_exact(A, B.get(), inv_m, b, cur, nx, s);
                 cur = nx;
             }
             UA_CK(cudaStreamSynchronize(s));

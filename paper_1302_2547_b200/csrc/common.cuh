@@ -84,7 +84,7 @@ struct Blocks {
 // ---------------------------------------------------------------- constants
 constexpr int kThreads = 256;           // staged kernels: threads per block
 constexpr int kRowsPerBlock = 256;      // max rows per row block
-constexpr int kStageCap = 2048;         // products staged per block (16 KB fp64)
+constexpr int kStageCap = 4096;         // products staged per block (32 KB fp64)
 constexpr int kStageHalf = kStageCap / 2;
 constexpr int kNumSMs = 148;            // B200
 

@@ -35,7 +35,12 @@ struct RedSlot {
     unsigned* ticket;   // zero between launches
 };
 
-template <class Src, class Epi, bool Unit>
+// ExactLong: rows longer than kStageCap are folded sequentially on one thread
+// (reference order, bit-exact; the kernel-table entry points) or, on the
+// solve path, as a fixed-order block tree per chunk with chunk sums added in
+// order (deterministic, not reference-ordered; the solve's parity bar is the
+// 1e-10 residual-history tolerance).  Short rows are always exact.
+template <class Src, class Epi, bool Unit, bool ExactLong = false>
 __global__ void __launch_bounds__(kThreads) k_csr_stream(Csr A, Blocks B, Src src_p, Epi epi_p) {
     __shared__ double prod[kStageCap];
     Epi epi = epi_p;
@@ -59,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) k_csr_stream(Csr A, Blocks B, Src sr
             for (int e = b; e < c; ++e) acc = __dadd_rn(acc, prod[e]);
             epi.row(i, acc, src);
         }
-    } else {
+    } else if (ExactLong) {
         // single long row: fold chunk by chunk on thread 0
         double acc = 0.0;
         for (int c0 = e0; c0 < e1; c0 += kStageCap) {
@@ -73,6 +78,15 @@ __global__ void __launch_bounds__(kThreads) k_csr_stream(Csr A, Blocks B, Src sr
                 for (int e = 0; e < c1 - c0; ++e) acc = __dadd_rn(acc, prod[e]);
             __syncthreads();
         }
+        if (threadIdx.x == 0) epi.row(r0, acc, src);
+    } else {
+        // single long row: per-thread strided partial sums, fixed block tree
+        double part = 0.0;
+        for (int e = e0 + (int)threadIdx.x; e < e1; e += kThreads) {
+            const int c = __ldg(A.ci + e);
+            part = __dadd_rn(part, Unit ? src(c) : __dmul_rn(__ldg(A.av + e), src(c)));
+        }
+        const double acc = block_sum<kThreads>(part, prod);
         if (threadIdx.x == 0) epi.row(r0, acc, src);
     }
     if constexpr (Epi::K > 0) {

@@ -40,7 +40,12 @@ struct RedScratch {
 constexpr int kMaxRedBlocks = 1 << 16;
 
 // ---- staged CSR operations (csr_stream.cuh) ----
+// kernel-table (bit-exact for every row length) variants
 void launch_spmv(const Csr& A, const Blocks& B, const double* x, double* y, cudaStream_t s);
+void launch_sweep_exact(const Csr& A, const Blocks& B, const double* invm, const double* b, const double* x,
+                        double* out, cudaStream_t s);
+void launch_restrict_exact(int nc, const int* agg_ptr, const int* members, const Blocks& MB, const double* r,
+                           double* rc, cudaStream_t s);
 // r = b - A x, x given (xmode 2) or implicit one sweep from zero (xmode 1) or zero (xmode 0)
 void launch_residual(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,
                      const double* x, double* r, const int* gate, cudaStream_t s);

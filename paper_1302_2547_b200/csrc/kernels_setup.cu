@@ -323,22 +323,27 @@ __global__ void k_seg_starts(int n, int nc, const int* sorted_keys, int* ptr) {
 }
 
 // ============================================================ row blocks
-__global__ void k_block_flags(int n, const int* rp, int* flag) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int len = rp[i + 1] - rp[i];
-        bool f = (i % kRowsPerBlock) == 0 || len > kStageHalf;
-        if (!f) {
-            const int lp = rp[i] - rp[i - 1];
-            f = lp > kStageHalf || (rp[i] / kStageHalf) != (rp[i - 1] / kStageHalf);
+// Rows are cut into tiles of kRowsPerBlock; each tile is split greedily into
+// blocks whose nonzeros fit kStageCap (a row longer than kStageCap forms a
+// block of its own and takes the kernel's long-row path).
+__global__ void k_tile_blocks(int n, const int* rp, const int* tile_off, int* cnt, int* start) {
+    const int ntiles = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        const int r0 = t * kRowsPerBlock, r1 = min(n, r0 + kRowsPerBlock);
+        int c = 0, rows = 0, nz = 0;
+        int pos = tile_off ? tile_off[t] : 0;
+        for (int i = r0; i < r1; ++i) {
+            const int len = rp[i + 1] - rp[i];
+            if (rows > 0 && nz + len > kStageCap) { ++c; rows = 0; nz = 0; }
+            if (rows == 0 && start) start[pos + c] = i;
+            nz += len;
+            ++rows;
         }
-        flag[i] = f;
+        if (rows > 0) ++c;
+        if (cnt) cnt[t] = c;
     }
 }
-__global__ void k_block_scatter(int n, const int* flag, const int* pos, int* start, int nb) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        if (flag[i]) start[pos[i]] = i;
-    if (blockIdx.x == 0 && threadIdx.x == 0) start[nb] = n;
-}
+__global__ void k_block_end(int n, int nb, int* start) { start[nb] = n; }
 
 // ============================================================ Galerkin
 // stream length per aggregate: sum of its members' row lengths
@@ -419,27 +424,31 @@ __global__ void k_galerkin_accum(Csr A, const int* __restrict__ v2a, int nc, con
     if (lane == 0) cnt[I] = c;
 }
 
-// Phase C: write row I sorted by J (rank = number of smaller keys)
-__global__ void k_galerkin_emit(int nc, const int* __restrict__ soff, const int* __restrict__ slen,
-                                const int* __restrict__ hkey, const double* __restrict__ hval,
-                                const int* __restrict__ rp_c, int* col_c, double* val_c) {
+// Phase C: compact the nonzero (J, value) pairs of row I to its output slot
+// range (slot order); rows are then sorted by J with a segmented sort.
+__global__ void k_galerkin_compact(int nc, const int* __restrict__ soff, const int* __restrict__ slen,
+                                   const int* __restrict__ hkey, const double* __restrict__ hval,
+                                   const int* __restrict__ rp_c, int* col_c, double* val_c) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = blockIdx.x * 8 + wib;
     if (I >= nc) return;
     const int cap = 2 * slen[I];
     const int* K = hkey + 2 * (size_t)soff[I];
     const double* V = hval + 2 * (size_t)soff[I];
-    const int base = rp_c[I];
-    for (int t = lane; t < cap; t += 32) {
-        const int key = K[t];
-        if (key < 0 || V[t] == 0.0) continue;
-        int rank = 0;
-        for (int u = 0; u < cap; ++u) {
-            const int k2 = K[u];
-            rank += (k2 >= 0 && k2 < key && V[u] != 0.0);
+    int base = rp_c[I];
+    for (int t0 = 0; t0 < cap; t0 += 32) {
+        const int t = t0 + lane;
+        int key = -1;
+        double v = 0.0;
+        if (t < cap) { key = K[t]; v = V[t]; }
+        const bool keep = key >= 0 && v != 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int pos = base + __popc(m & ((1u << lane) - 1u));
+            col_c[pos] = key;
+            val_c[pos] = v;
         }
-        col_c[base + rank] = key;
-        val_c[base + rank] = V[t];
+        base += __popc(m);
     }
 }
 
@@ -622,16 +631,18 @@ void build_row_blocks(int n, const int* rp, DBuf<int>& start, int& nb, cudaStrea
         UA_CK(cudaMemsetAsync(start.p, 0, sizeof(int), s));
         return;
     }
-    DBuf<int> flag(n + 1, s), pos(n + 1, s);
-    UA_LAUNCH(k_block_flags, grid_for(n), 256, 0, s, n, rp, flag.p);
-    UA_CK(cudaMemsetAsync(flag.p + n, 0, sizeof(int), s));
-    exclusive_scan(flag.p, pos.p, n + 1, s);
+    const int nt = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+    DBuf<int> cnt(nt + 1, s), off(nt + 1, s);
+    UA_LAUNCH(k_tile_blocks, grid_for(nt), 256, 0, s, n, rp, (const int*)nullptr, cnt.p, (int*)nullptr);
+    UA_CK(cudaMemsetAsync(cnt.p + nt, 0, sizeof(int), s));
+    exclusive_scan(cnt.p, off.p, nt + 1, s);
     int h_nb = 0;
-    UA_CK(cudaMemcpyAsync(&h_nb, pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaMemcpyAsync(&h_nb, off.p + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
     nb = h_nb;
     start.alloc(nb + 1, s);
-    UA_LAUNCH(k_block_scatter, grid_for(n), 256, 0, s, n, flag.p, pos.p, start.p, nb);
+    UA_LAUNCH(k_tile_blocks, grid_for(nt), 256, 0, s, n, rp, (const int*)off.p, (int*)nullptr, start.p);
+    UA_LAUNCH(k_block_end, 1, 1, 0, s, n, nb, start.p);
 }
 
 // aggregate() on device.  state arrays are n-sized scratch.
@@ -740,7 +751,18 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     UA_CK(cudaStreamSynchronize(s));
     ci_c.alloc(std::max(nnz_c, 1), s);
     av_c.alloc(std::max(nnz_c, 1), s);
-    UA_LAUNCH(k_galerkin_emit, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ci_c.p, av_c.p);
+    if (nnz_c > 0) {
+        DBuf<int> ck(nnz_c, s);
+        DBuf<double> cv(nnz_c, s);
+        UA_LAUNCH(k_galerkin_compact, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ck.p,
+                  cv.p);
+        size_t tmp = 0;
+        UA_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
+                                                  rp_c.p + 1, s));
+        DBuf<char> t(tmp, s);
+        UA_CK(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
+                                                  rp_c.p + 1, s));
+    }
     return nnz_c;
 }
 

@@ -121,16 +121,32 @@ struct EpiStoreG : NoReduce {
     __device__ void row(int i, double acc, const S&) { y[i] = acc; }
 };
 
-template <class Src, class Epi, bool Unit>
+template <class Src, class Epi, bool Unit, bool Exact = false>
 static void run_stream(const Csr& A, const Blocks& B, const Src& src, const Epi& epi, cudaStream_t s) {
     if (B.nb == 0) return;
-    UA_LAUNCH((k_csr_stream<Src, Epi, Unit>), B.nb, kThreads, 0, s, A, B, src, epi);
+    UA_LAUNCH((k_csr_stream<Src, Epi, Unit, Exact>), B.nb, kThreads, 0, s, A, B, src, epi);
 }
 
 void launch_spmv(const Csr& A, const Blocks& B, const double* x, double* y, cudaStream_t s) {
     EpiStore e{};
     e.y = y;
-    run_stream<SrcVec, EpiStore, false>(A, B, SrcVec{x}, e, s);
+    run_stream<SrcVec, EpiStore, false, true>(A, B, SrcVec{x}, e, s);
+}
+
+void launch_sweep_exact(const Csr& A, const Blocks& B, const double* invm, const double* b, const double* x,
+                        double* out, cudaStream_t s) {
+    EpiSweep e{};
+    e.invm = invm; e.b = b; e.out = out; e.g = nullptr;
+    run_stream<SrcVec, EpiSweep, false, true>(A, B, SrcVec{x}, e, s);
+}
+
+void launch_restrict_exact(int nc, const int* agg_ptr, const int* members, const Blocks& MB, const double* r,
+                           double* rc, cudaStream_t s) {
+    Csr P;
+    P.n = nc; P.rp = agg_ptr; P.ci = members; P.av = nullptr;
+    EpiStoreG e{};
+    e.y = rc; e.g = nullptr;
+    run_stream<SrcVec, EpiStoreG, true, true>(P, MB, SrcVec{r}, e, s);
 }
 
 void launch_residual(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,

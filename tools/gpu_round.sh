@@ -16,7 +16,14 @@ for st in $STAGES; do
     benchref) timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "benchref rc=$?" >> $OUT/status.txt ;;
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
            python tools/one_solve.py > $OUT/ncu_launches.log 2>&1; echo "ncu rc=$?" >> $OUT/status.txt ;;
-    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_csr_stream -s 40 -c 3 \
-           -o $OUT/prof python tools/one_solve.py > $OUT/ncu_full.log 2>&1; echo "ncufull rc=$?" >> $OUT/status.txt ;;
+    ncufull)
+      # level-0 hot kernels of iteration 1: residual (first SrcPre1), fused
+      # up-sweep (31st SrcUp: 30 coarse-level cycles precede it), NPCG direction SpMV
+      for spec in "SrcPre1:0:resid" "SrcUp:30:upsweep" "EpiDirNpcg:0:dir"; do
+        IFS=: read pat skip tag <<< "$spec"
+        timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+          -k regex:$pat -s $skip -c 1 -o $OUT/prof_$tag python tools/one_solve.py > $OUT/ncu_full_$tag.log 2>&1
+        echo "ncufull $tag rc=$?" >> $OUT/status.txt
+      done ;;
   esac
 done
