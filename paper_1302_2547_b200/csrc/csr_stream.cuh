@@ -53,9 +53,24 @@ __global__ void __launch_bounds__(kThreads) k_csr_stream(Csr A, Blocks B, Src sr
     const int r0 = B.start[blockIdx.x], r1 = B.start[blockIdx.x + 1];
     const int e0 = A.rp[r0], e1 = A.rp[r1];
     if (e1 - e0 <= kStageCap) {
-        for (int e = e0 + (int)threadIdx.x; e < e1; e += kThreads) {
-            const int c = __ldg(A.ci + e);
-            prod[e - e0] = Unit ? src(c) : __dmul_rn(__ldg(A.av + e), src(c));
+        // batches of kUnroll entries per thread: all index/value loads first,
+        // then all gathers, so each warp keeps ~3*kUnroll loads in flight
+        for (int base = e0 + (int)threadIdx.x; base < e1; base += kThreads * kUnroll) {
+            int c[kUnroll];
+            double a[kUnroll], v[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int e = base + u * kThreads;
+                c[u] = e < e1 ? __ldg(A.ci + e) : -1;
+                if (!Unit) a[u] = e < e1 ? __ldg(A.av + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) v[u] = c[u] >= 0 ? src(c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int e = base + u * kThreads;
+                if (e < e1) prod[e - e0] = Unit ? v[u] : __dmul_rn(a[u], v[u]);
+            }
         }
         __syncthreads();
         for (int i = r0 + (int)threadIdx.x; i < r1; i += kThreads) {

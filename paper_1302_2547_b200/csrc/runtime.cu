@@ -612,16 +612,20 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
 // ====================================================================== C ABI
 using namespace uaamg;
 
-#define UA_GUARD(...)                                           \
-    try {                                                       \
-        __VA_ARGS__;                                                 \
-        return UAAMG_OK;                                        \
-    } catch (const Error& e) {                                  \
-        g_last_error = e.what();                                \
-        return e.code;                                          \
-    } catch (const std::exception& e) {                         \
-        g_last_error = e.what();                                \
-        return UAAMG_ECUDA;                                     \
+#define UA_GUARD(...)                                                                        \
+    try {                                                                                    \
+        __VA_ARGS__;                                                                         \
+        const cudaError_t pe_ = cudaGetLastError();                                          \
+        if (pe_ != cudaSuccess)                                                              \
+            throw Error(UAAMG_ECUDA, std::string("pending CUDA error after ") + __func__ + ": " + \
+                                         cudaGetErrorString(pe_));                           \
+        return UAAMG_OK;                                                                     \
+    } catch (const Error& e) {                                                               \
+        g_last_error = e.what();                                                             \
+        return e.code;                                                                       \
+    } catch (const std::exception& e) {                                                      \
+        g_last_error = e.what();                                                             \
+        return UAAMG_ECUDA;                                                                  \
     }
 
 extern "C" {
