@@ -265,7 +265,9 @@ struct Plan {
     cudaStream_t s;
     int prof = -1;  // >= 0: record level-0 timing events of this parity
     void mark(int k) {
-        if (prof >= 0) UA_CK(cudaEventRecord(ws->pev[prof][k], s));
+        // External: a real event-record node inside the captured graph (a
+        // plain cudaEventRecord during capture only orders nodes)
+        if (prof >= 0) UA_CK(cudaEventRecordWithFlags(ws->pev[prof][k], s, cudaEventRecordExternal));
     }
     RedScratch rs() const { return RedScratch{ws->partials.p, ws->ticket.p}; }
     int coarsest() const { return (int)h->levels.size() - 1; }
@@ -534,6 +536,8 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
             float t = 0;
             if (cudaEventElapsedTime(&t, ws->pev[par][2 * k], ws->pev[par][2 * k + 1]) == cudaSuccess)
                 prof_s[k] += t * 1e-3;
+            else
+                (void)cudaGetLastError();  // not recorded in this replay: skip, clear
         }
         ++prof_n;
     };
