@@ -88,6 +88,7 @@ constexpr int kStageCap = 4096;         // products staged per block (32 KB fp64
 constexpr int kStageHalf = kStageCap / 2;
 constexpr int kNumSMs = 148;            // B200
 constexpr int kUnroll = 4;              // staged-load batch per thread
+constexpr int kLongRow = 64;            // setup kernels: rows longer than this get a warp
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 

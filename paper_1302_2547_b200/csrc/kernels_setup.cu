@@ -6,9 +6,13 @@
 //
 // Reference: U/aggregation.py:130-203, U/hierarchy.py:22-65,
 // K/numba_backend.py:14-44 (hash), :100-111 (scores), :145-273.
+#include <cooperative_groups.h>
+#include <cstring>
 #include <cub/cub.cuh>
 
 #include "setup.h"
+
+namespace cg = cooperative_groups;
 
 namespace uaamg {
 
@@ -294,6 +298,197 @@ __global__ void k_capped_commit(int n, uint8_t* st, uint8_t* newly, int* remaini
     if (local) atomicAdd(remaining, local);
 }
 
+// ============================================================ cooperative aggregation
+// The whole multi-pass PAA of one level (U/aggregation.py:184-194) in one
+// cooperative launch: scores -> max-hop -> select -> max-hop -> claim ->
+// admission fixpoint -> commit, separated by grid-wide barriers, with the
+// pass / admission loop control read from device counters (no host round
+// trips).  Short rows are handled thread-per-row, rows longer than kLongRow
+// warp-per-row (key max and "any" are order-free, so results are identical).
+struct AggCoop {
+    Csr A;
+    const int* deg;
+    uint64_t seed;
+    int max_passes;
+    uint8_t* st;
+    double* sc;
+    double* ms;
+    int* mi;
+    int* owner;
+    uint8_t* adm;
+    int* seed_of;
+    int* ctl;  // [0..2] centers / pass slot, [3..5] remaining / pass slot, [6..8] changed / iteration slot, [9] passes, [10] leftover
+};
+
+__device__ __forceinline__ void warp_keymax(double& s, int& i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+        if (i2 >= 0 && (i < 0 || key_gt(s2, i2, s, i))) { s = s2; i = i2; }
+    }
+}
+
+// max key over row r of the hop-1 table (ms, mi); lanes split the row when warp
+__device__ __forceinline__ void row_hopmax(const Csr& A, const double* ms, const int* mi, int r, int e0, int e1,
+                                           int step, double& bs, int& bi) {
+    for (int e = e0; e < e1; e += step) {
+        const int k = __ldg(A.ci + e);
+        const int c = mi[k];
+        if (c < 0) continue;
+        const double v = ms[k];
+        if (bi < 0 || key_gt(v, c, bs, bi)) { bs = v; bi = c; }
+    }
+}
+
+__device__ void coop_hop1(const AggCoop& g, int mode, int tid, int nth, int lane, int w, int nw) {
+    const Csr& A = g.A;
+    for (int k = tid; k < A.n; k += nth) {
+        const int e0 = A.rp[k], e1 = A.rp[k + 1];
+        if (e1 - e0 > kLongRow) continue;
+        double bs = 0.0;
+        int bi = -1;
+        for (int e = e0; e < e1; ++e) {
+            const int j = __ldg(A.ci + e);
+            const uint8_t sj = g.st[j];
+            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
+            const double v = g.sc[j];
+            if (bi < 0 || key_gt(v, j, bs, bi)) { bs = v; bi = j; }
+        }
+        g.ms[k] = bs;
+        g.mi[k] = bi;
+    }
+    for (int k = w; k < A.n; k += nw) {
+        const int e0 = A.rp[k], e1 = A.rp[k + 1];
+        if (e1 - e0 <= kLongRow) continue;
+        double bs = 0.0;
+        int bi = -1;
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const int j = __ldg(A.ci + e);
+            const uint8_t sj = g.st[j];
+            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
+            const double v = g.sc[j];
+            if (bi < 0 || key_gt(v, j, bs, bi)) { bs = v; bi = j; }
+        }
+        warp_keymax(bs, bi);
+        if (lane == 0) { g.ms[k] = bs; g.mi[k] = bi; }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
+    cg::grid_group grid = cg::this_grid();
+    const Csr& A = g.A;
+    const int n = A.n;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, w = tid >> 5, nw = nth >> 5;
+    volatile int* ctl = g.ctl;
+    int remaining = n, pass = 0, itg = 0;
+    for (; pass < g.max_passes; ++pass) {
+        if (remaining == 0) break;  // U/aggregation.py:186
+        const int ps = pass % 3;
+        if (tid == 0) { ctl[(pass + 1) % 3] = 0; ctl[3 + (pass + 1) % 3] = 0; }
+        // scores (K/numba_backend.py:100-111)
+        const uint64_t base = pass_base(g.seed, pass);
+        for (int i = tid; i < n; i += nth) {
+            const double u = hash_unit(base, i);
+            g.sc[i] = __dadd_rn((double)g.deg[i], __ddiv_rn(__dadd_rn((double)(i % 12), u), 12.0));
+        }
+        grid.sync();
+        coop_hop1(g, 0, tid, nth, lane, w, nw);
+        grid.sync();
+        // selection (K/numba_backend.py:175-193)
+        int local = 0;
+        for (int i = tid; i < n; i += nth) {
+            const int e0 = A.rp[i], e1 = A.rp[i + 1];
+            if (e1 - e0 > kLongRow || g.st[i] != 0) continue;
+            double bs = 0.0;
+            int bi = -1;
+            row_hopmax(A, g.ms, g.mi, i, e0, e1, 1, bs, bi);
+            if (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi)) { g.st[i] = 1; ++local; }
+        }
+        for (int i = w; i < n; i += nw) {
+            const int e0 = A.rp[i], e1 = A.rp[i + 1];
+            if (e1 - e0 <= kLongRow || g.st[i] != 0) continue;
+            double bs = 0.0;
+            int bi = -1;
+            row_hopmax(A, g.ms, g.mi, i, e0 + lane, e1, 32, bs, bi);
+            warp_keymax(bs, bi);
+            if (lane == 0 && (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi))) { g.st[i] = 1; ++local; }
+        }
+        if (local) atomicAdd((int*)&ctl[ps], local);
+        grid.sync();
+        coop_hop1(g, 1, tid, nth, lane, w, nw);
+        grid.sync();
+        // claim (K/numba_backend.py:196-220) + admission seeds
+        for (int j = tid; j < n; j += nth) {
+            const int e0 = A.rp[j], e1 = A.rp[j + 1];
+            const uint8_t sj = g.st[j];
+            g.adm[j] = (sj == 1);
+            if (sj == 1) { g.owner[j] = j; continue; }
+            if (sj == 2) { g.owner[j] = -1; continue; }
+            if (e1 - e0 > kLongRow) continue;
+            double bs = 0.0;
+            int bi = -1;
+            row_hopmax(A, g.ms, g.mi, j, e0, e1, 1, bs, bi);
+            g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
+        }
+        for (int j = w; j < n; j += nw) {
+            const int e0 = A.rp[j], e1 = A.rp[j + 1];
+            if (e1 - e0 <= kLongRow || g.st[j] != 0) continue;
+            double bs = 0.0;
+            int bi = -1;
+            row_hopmax(A, g.ms, g.mi, j, e0 + lane, e1, 32, bs, bi);
+            warp_keymax(bs, bi);
+            if (lane == 0) g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
+        }
+        grid.sync();
+        // admission fixpoint (uncapped sweeps of K/numba_backend.py:235-273)
+        volatile uint8_t* adm = g.adm;
+        while (true) {
+            const int slot = itg % 3;
+            if (tid == 0) ctl[6 + (itg + 1) % 3] = 0;
+            int ch = 0;
+            for (int j = tid; j < n; j += nth) {
+                const int c = g.owner[j];
+                const int e0 = A.rp[j], e1 = A.rp[j + 1];
+                if (c < 0 || c == j || adm[j] || e1 - e0 > kLongRow) continue;
+                for (int e = e0; e < e1; ++e) {
+                    const int nb = __ldg(A.ci + e);
+                    if (adm[nb] && g.owner[nb] == c) { adm[j] = 1; ch = 1; break; }
+                }
+            }
+            for (int j = w; j < n; j += nw) {
+                const int c = g.owner[j];
+                const int e0 = A.rp[j], e1 = A.rp[j + 1];
+                if (c < 0 || c == j || adm[j] || e1 - e0 <= kLongRow) continue;
+                bool f = false;
+                for (int e = e0 + lane; e < e1 && !f; e += 32) {
+                    const int nb = __ldg(A.ci + e);
+                    f = adm[nb] && g.owner[nb] == c;
+                }
+                if (__any_sync(0xffffffffu, f) && lane == 0) { adm[j] = 1; ch = 1; }
+            }
+            if (ch) atomicOr((int*)&ctl[6 + slot], 1);
+            grid.sync();
+            const int any = ctl[6 + slot];
+            ++itg;
+            if (!any) break;
+        }
+        // commit: admitted vertices and centers are processed, seeded by owner
+        int left = 0;
+        for (int j = tid; j < n; j += nth) {
+            const uint8_t sj = g.st[j];
+            if (sj == 1 || (sj == 0 && adm[j])) { g.seed_of[j] = g.owner[j]; g.st[j] = 2; }
+            else if (sj == 0) ++left;
+        }
+        if (left) atomicAdd((int*)&ctl[3 + ps], left);
+        grid.sync();
+        remaining = ctl[3 + ps];
+        if (ctl[ps] == 0) { ++pass; break; }  // no centers (cannot happen, U/aggregation.py:190)
+    }
+    if (tid == 0) { ctl[9] = pass; ctl[10] = remaining; }
+}
+
 // ============================================================ renumbering
 // leftovers become singletons (U/aggregation.py:195-198); seed flags
 __global__ void k_finish_seeds(int n, const uint8_t* st, int* seed_of, int* flag) {
@@ -422,6 +617,70 @@ __global__ void k_galerkin_accum(Csr A, const int* __restrict__ v2a, int nc, con
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) cnt[I] = c;
+}
+
+// Order-free Galerkin accumulation, valid when every value of A is an
+// integer and nnz * max|a| < 2^52: then every partial sum of every (I,J) entry
+// is an exactly representable integer, so any summation order (here: parallel
+// atomics) gives the bit-identical result of the reference's sequential sum.
+__device__ __forceinline__ void gal_insert_add(int* K, double* V, int cap, int J, double a) {
+    unsigned slot = hslot(J, cap);
+    while (true) {
+        const int prev = atomicCAS(K + slot, -1, J);
+        if (prev == -1 || prev == J) break;
+        slot = (slot + 1 == (unsigned)cap) ? 0u : slot + 1;
+    }
+    atomicAdd(V + slot, a);
+}
+__global__ void k_galerkin_accum_int(Csr A, const int* __restrict__ v2a, const int* __restrict__ soff,
+                                     const int* __restrict__ slen, int* hkey, double* hval) {
+    // short rows: one thread per row; rows longer than kLongRow: one warp per row
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int r = tid; r < A.n; r += nth) {
+        const int e0 = A.rp[r], e1 = A.rp[r + 1];
+        if (e1 - e0 > kLongRow) continue;
+        const int I = v2a[r];
+        const int cap = 2 * slen[I];
+        int* K = hkey + 2 * (size_t)soff[I];
+        double* V = hval + 2 * (size_t)soff[I];
+        for (int e = e0; e < e1; ++e) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+    }
+    const int lane = threadIdx.x & 31, w = tid >> 5, nw = nth >> 5;
+    for (int r = w; r < A.n; r += nw) {
+        const int e0 = A.rp[r], e1 = A.rp[r + 1];
+        if (e1 - e0 <= kLongRow) continue;
+        const int I = v2a[r];
+        const int cap = 2 * slen[I];
+        int* K = hkey + 2 * (size_t)soff[I];
+        double* V = hval + 2 * (size_t)soff[I];
+        for (int e = e0 + lane; e < e1; e += 32) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+    }
+}
+__global__ void k_galerkin_count(int nc, const int* __restrict__ soff, const int* __restrict__ slen,
+                                 const int* __restrict__ hkey, const double* __restrict__ hval, int* cnt) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int I = blockIdx.x * 8 + wib;
+    if (I >= nc) return;
+    const int cap = 2 * slen[I];
+    const int* K = hkey + 2 * (size_t)soff[I];
+    const double* V = hval + 2 * (size_t)soff[I];
+    int c = 0;
+    for (int t = lane; t < cap; t += 32) c += (K[t] >= 0 && V[t] != 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[I] = c;
+}
+// integrality test for the order-free path
+__global__ void k_int_check(long long m, const double* __restrict__ v, int* nonint, unsigned long long* maxabs) {
+    double mx = 0.0;
+    int bad = 0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m; k += (long long)gridDim.x * blockDim.x) {
+        const double a = v[k];
+        bad |= (a != rint(a));
+        mx = fmax(mx, fabs(a));
+    }
+    if (bad) atomicOr(nonint, 1);
+    atomicMax(maxabs, (unsigned long long)__double_as_longlong(mx));
 }
 
 // Phase C: compact the nonzero (J, value) pairs of row I to its output slot
@@ -656,8 +915,8 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
     DBuf<int> mi(n, s), owner(n, s), seed_of(n, s), counters(4, s);
     UA_CK(cudaMemsetAsync(st.p, 0, n, s));
     UA_CK(cudaMemsetAsync(seed_of.p, 0xff, sizeof(int) * n, s));
-    int* h_cnt = nullptr;
-    UA_CK(cudaMallocHost(&h_cnt, 4 * sizeof(int)));
+    static thread_local int* h_cnt = nullptr;  // pinned, reused across calls
+    if (!h_cnt) UA_CK(cudaMallocHost(&h_cnt, 4 * sizeof(int)));
     const bool capped = size_cap > 0;
     DBuf<int> bcnt, bptr, bjs, ord, cursor;
     DBuf<double> bw;
@@ -669,6 +928,30 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
     }
     int passes = 0;
     int remaining = n;
+    if (!capped) {
+        DBuf<int> ctl(16, s);
+        UA_CK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(int), s));
+        AggCoop g;
+        g.A = A; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
+        g.mi = mi.p; g.owner = owner.p; g.adm = adm.p; g.seed_of = seed_of.p; g.ctl = ctl.p;
+        static int max_blocks = 0;
+        if (!max_blocks) {
+            int per_sm = 0, dev = 0, sms = 0;
+            UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aggregate_coop, 256, 0));
+            UA_CK(cudaGetDevice(&dev));
+            UA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            max_blocks = std::max(1, per_sm) * sms;
+        }
+        const int blocks = std::max(1, std::min(max_blocks, cdiv(n, 256)));
+        void* args[] = {&g};
+        UA_CK(cudaLaunchCooperativeKernel((void*)k_aggregate_coop, blocks, 256, args, 0, s));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        UA_CK(cudaMemcpyAsync(h_cnt, ctl.p + 9, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        passes = h_cnt[0];
+        remaining = h_cnt[1];
+        max_passes = 0;  // skip the host-driven loop below
+    }
     for (int pass = 0; pass < max_passes; ++pass) {
         if (remaining == 0) break;  // U/aggregation.py:186
         UA_CK(cudaMemsetAsync(counters.p, 0, 4 * sizeof(int), s));
@@ -703,7 +986,6 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         remaining = h_cnt[2];
         if (h_cnt[0] == 0) break;  // no centers: cannot happen (U/aggregation.py:190)
     }
-    cudaFreeHost(h_cnt);
     // leftovers + renumber
     DBuf<int> flag(n + 1, s), rank(n + 1, s);
     UA_LAUNCH(k_finish_seeds, G, 256, 0, s, n, st.p, seed_of.p, flag.p);
@@ -729,6 +1011,24 @@ void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cu
     UA_LAUNCH(k_seg_starts, grid_for(n), 256, 0, s, n, nc, keys_out.p, agg_ptr);
 }
 
+// true when every value is an integer and nnz * max|a| < 2^52 (exact in any order)
+static bool integer_exact(const Csr& A, cudaStream_t s) {
+    if (A.nnz == 0) return true;
+    DBuf<int> bad(1, s);
+    DBuf<unsigned long long> mx(1, s);
+    UA_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    UA_CK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
+    UA_LAUNCH(k_int_check, grid_for(A.nnz), 256, 0, s, (long long)A.nnz, A.av, bad.p, mx.p);
+    int h_bad = 0;
+    unsigned long long h_mx = 0;
+    UA_CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaMemcpyAsync(&h_mx, mx.p, sizeof(h_mx), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    double m;
+    std::memcpy(&m, &h_mx, 8);
+    return h_bad == 0 && (double)A.nnz * m < 4503599627370496.0;  // 2^52
+}
+
 // Galerkin: returns nnz_c; allocates out arrays
 long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
                           DBuf<int>& rp_c, DBuf<int>& ci_c, DBuf<double>& av_c, cudaStream_t s) {
@@ -741,8 +1041,13 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     DBuf<double> hval(hsz, s);
     UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
     UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
-    UA_LAUNCH(k_galerkin_accum, cdiv(nc, 8), 256, 0, s, A, v2a, nc, agg_ptr, members, soff.p, slen.p, hkey.p,
-              hval.p, cnt.p);
+    if (integer_exact(A, s)) {
+        UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, v2a, soff.p, slen.p, hkey.p, hval.p);
+        UA_LAUNCH(k_galerkin_count, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, cnt.p);
+    } else {
+        UA_LAUNCH(k_galerkin_accum, cdiv(nc, 8), 256, 0, s, A, v2a, nc, agg_ptr, members, soff.p, slen.p, hkey.p,
+                  hval.p, cnt.p);
+    }
     UA_CK(cudaMemsetAsync(cnt.p + nc, 0, sizeof(int), s));
     rp_c.alloc(nc + 1, s);
     exclusive_scan(cnt.p, rp_c.p, nc + 1, s);

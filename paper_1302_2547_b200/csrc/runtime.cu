@@ -203,6 +203,19 @@ static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t 
 static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
                                    const uaamg_setup_params& P, cudaStream_t s) {
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
+    static bool pool_configured = false;
+    if (!pool_configured) {
+        // keep freed blocks in the stream-ordered pool: setup allocates and
+        // frees O(nnz) scratch per level; returning it to the driver on every
+        // synchronize costs milliseconds per setup
+        int dev = 0;
+        cudaMemPool_t pool;
+        UA_CK(cudaGetDevice(&dev));
+        UA_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        UA_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        pool_configured = true;
+    }
     auto h = std::make_unique<uaamg_hierarchy>();
     UA_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     StreamJoin join(s, h->stream);
