@@ -171,6 +171,9 @@ typedef struct {
     int max_iters;           /* npcg_solve max_iters                          */
     int use_graphs;          /* 1: replay one CUDA graph per iteration        */
     int profile_level0;      /* 1: time level-0 smoother kernels (events)     */
+    int engine_rows;         /* levels >= 1 with at most this many rows run in
+                                the persistent coarse engine (one cooperative
+                                launch per cycle entry); 0 off, < 0 default   */
 } uaamg_solve_params;
 
 typedef struct {

@@ -8,13 +8,6 @@
 namespace uaamg {
 extern thread_local std::string g_last_error;
 
-struct RowBlocksTmp {
-    DBuf<int> start;
-    int nb = 0;
-    RowBlocksTmp(int n, const int* rp, cudaStream_t s) { build_row_blocks(n, rp, start, nb, s); }
-    Blocks get() const { return Blocks{nb, start.p}; }
-};
-
 static Csr make_csr(int n, const int* rp, const int* ci, const double* av) {
     Csr c;
     c.n = n; c.rp = rp; c.ci = ci; c.av = av;
@@ -54,8 +47,7 @@ int uaamg_k_spmv(int n, const int* row_ptr, const int* col, const double* val, c
                  void* stream) {
     UA_GUARD({
         cudaStream_t s = (cudaStream_t)stream;
-        RowBlocksTmp B(n, row_ptr, s);
-        launch_spmv(make_csr(n, row_ptr, col, val), B.get(), x, y, s);
+        launch_spmv(make_csr(n, row_ptr, col, val), exact_groups(n), x, y, s);
     })
 }
 
@@ -146,8 +138,7 @@ int uaamg_k_galerkin(int n, const int* row_ptr, const int* col, const double* va
 int uaamg_k_restrict(int nc, const int* agg_ptr, const int* members, const double* r, double* out, void* stream) {
     UA_GUARD({
         cudaStream_t s = (cudaStream_t)stream;
-        RowBlocksTmp B(nc, agg_ptr, s);
-        launch_restrict_exact(nc, agg_ptr, members, B.get(), r, out, s);
+        launch_restrict_exact(nc, agg_ptr, members, exact_groups(nc), r, out, s);
     })
 }
 
@@ -164,13 +155,12 @@ int uaamg_k_smooth_sweeps(int n, const int* row_ptr, const int* col, const doubl
         if (sweeps <= 0) {
             UA_CK(cudaMemcpyAsync(out, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         } else {
-            RowBlocksTmp B(n, row_ptr, s);
             Csr A = make_csr(n, row_ptr, col, val);
             DBuf<double> t0(std::max(n, 1), s), t1(std::max(n, 1), s);
             const double* cur = x;
             for (int k = 0; k < sweeps; ++k) {
                 double* nx = (k == sweeps - 1) ? out : ((cur == t0.p) ? t1.p : t0.p);
-                launch_sweep_exact(A, B.get(), inv_m, b, cur, nx, s);
+                launch_sweep_exact(A, exact_groups(n), inv_m, b, cur, nx, s);
                 cur = nx;
             }
             UA_CK(cudaStreamSynchronize(s));

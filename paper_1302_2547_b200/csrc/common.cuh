@@ -75,19 +75,9 @@ struct Csr {
     const double* av = nullptr;
 };
 
-// Row-block partition for the smem-staged kernels (see csr_stream.cuh).
-struct Blocks {
-    int nb = 0;
-    const int* start = nullptr;  // nb+1 entries, start[nb] = n
-};
-
 // ---------------------------------------------------------------- constants
 constexpr int kThreads = 256;           // staged kernels: threads per block
-constexpr int kRowsPerBlock = 256;      // max rows per row block
-constexpr int kStageCap = 4096;         // products staged per block (32 KB fp64)
-constexpr int kStageHalf = kStageCap / 2;
 constexpr int kNumSMs = 148;            // B200
-constexpr int kUnroll = 4;              // staged-load batch per thread
 constexpr int kLongRow = 64;            // setup kernels: rows longer than this get a warp
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

@@ -1,0 +1,143 @@
+// csr_group.cuh -- warp-granular CSR row kernel for every SpMV-shaped solve
+// operation (residual, restriction, fused prolongation + sweep, direction
+// SpMV), used by the standalone launches and by the persistent engine.
+//
+// Work unit = one warp.  Units [0, ng) are row groups of 32 consecutive rows
+// (lane = row).  A group's nonzeros [rp[r0], rp[r0+32]) are contiguous, so
+// the warp streams them in rounds of kGrpRound entries with fully coalesced
+// loads -- all index/value loads of a round issued first, then all gathers
+// (kGrpU independent loads in flight per lane per stage) -- and stages the
+// products in a per-warp shared-memory window; each lane then folds the part
+// of its own row that lies in the window into its accumulator.  Rounds are
+// in ascending entry order, so every row is summed sequentially in ascending
+// k from 0.0 with rounded products (-fmad=false): bit-identical to the
+// reference's numba row loops (K/numba_backend.py:47-56, :276-285,
+// :297-310) for ANY row length.
+//
+// Units [ng, ng + np) are pieces of long rows (more than long_min entries,
+// solve path only): each piece sums <= kGrpRound entries with a warp tree,
+// stores its partial, and the last piece of a row to arrive (atomic ticket)
+// adds the row's partials in piece order and runs the epilogue --
+// deterministic, not reference-ordered (the solve's parity bar is the 1e-10
+// residual-history tolerance).  The lanes of the owning group skip such rows.
+#pragma once
+#include "solve_ops.cuh"
+
+namespace uaamg {
+
+constexpr int kGrpU = 8;                  // entries per lane per round
+constexpr int kGrpRound = 32 * kGrpU;     // 256 entries per round
+constexpr int kGrpWarps = 8;              // warps per CTA (launch path)
+constexpr int kGrpCtasPerSM = 8;          // launch path: grid cap = SMs x this (grid-stride over units)
+
+template <bool Unit, class Src>
+__device__ __forceinline__ double grp_prod(const Csr& A, const Src& src, int e) {
+    const int k = __ldg(A.ci + e);
+    return Unit ? src(k) : __dmul_rn(__ldg(A.av + e), src(k));
+}
+
+// One work unit.  win: this warp's kGrpRound-double shared window.
+template <bool Unit, class Src, class Epi>
+__device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, const Src& src, Epi& epi,
+                                         double* win) {
+    const int lane = threadIdx.x & 31;
+    if (u < G.ng) {
+        const int i = (u << 5) + lane;
+        const int rlast = min((u << 5) + 32, G.n);
+        const bool valid = i < G.n;
+        const int bi = valid ? __ldg(A.rp + i) : 0;
+        const int ei = valid ? __ldg(A.rp + i + 1) : 0;
+        const int e0 = __shfl_sync(0xffffffffu, bi, 0);
+        const int e1 = __ldg(A.rp + rlast);
+        const bool mine = valid && (ei - bi) <= G.long_min;
+        double acc = 0.0;
+        // stream [lo, hi) in rounds; each lane folds its row's part of a round
+        auto stream = [&](int lo, int hi) {
+            for (int base = lo; base < hi; base += kGrpRound) {
+                int c[kGrpU];
+                double a[kGrpU];
+#pragma unroll
+                for (int q = 0; q < kGrpU; ++q) {
+                    const int e = base + lane + 32 * q;
+                    c[q] = e < hi ? __ldg(A.ci + e) : -1;
+                    if (!Unit) a[q] = e < hi ? __ldg(A.av + e) : 0.0;
+                }
+                double v[kGrpU];
+#pragma unroll
+                for (int q = 0; q < kGrpU; ++q) v[q] = c[q] >= 0 ? src(c[q]) : 0.0;
+#pragma unroll
+                for (int q = 0; q < kGrpU; ++q) win[lane + 32 * q] = Unit ? v[q] : __dmul_rn(a[q], v[q]);
+                __syncwarp();
+                if (mine) {
+                    const int l0 = max(bi, base), l1 = min(ei, base + kGrpRound);
+                    for (int e = l0; e < l1; ++e) acc = __dadd_rn(acc, win[e - base]);
+                }
+                __syncwarp();
+            }
+        };
+        // long rows of this group are pieces: stream around them
+        unsigned lm = __ballot_sync(0xffffffffu, valid && !mine);
+        int lo = e0;
+        while (lm) {
+            const int L = __ffs(lm) - 1;
+            lm &= lm - 1;
+            stream(lo, __shfl_sync(0xffffffffu, bi, L));
+            lo = __shfl_sync(0xffffffffu, ei, L);
+        }
+        stream(lo, e1);
+        if (mine) epi.row(i, acc, src);
+    } else {
+        const int4 pc = G.piece[u - G.ng];
+        const int row = pc.x, eb = pc.y, ee = pc.z, lr = pc.w;
+        double part = 0.0;
+#pragma unroll
+        for (int q = 0; q < kGrpU; ++q) {
+            const int e = eb + lane + 32 * q;
+            if (e < ee) part = __dadd_rn(part, grp_prod<Unit>(A, src, e));
+        }
+        part = warp_sum(part);
+        const int p0 = G.pbase[lr], np = G.pbase[lr + 1] - p0;
+        const int slot = p0 + (eb - __ldg(A.rp + row)) / kGrpRound;
+        bool last = false;
+        if (lane == 0) {
+            G.part[slot] = part;
+            __threadfence();
+            last = atomicAdd(G.ticket + lr, 1u) == (unsigned)(np - 1);
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            __threadfence();
+            if (lane == 0) {
+                double acc = 0.0;
+                for (int k = 0; k < np; ++k) acc = __dadd_rn(acc, __ldcg(G.part + p0 + k));
+                G.ticket[lr] = 0u;
+                epi.row(row, acc, src);
+            }
+        }
+    }
+}
+
+// Launch-path kernel: one unit per warp, kGrpWarps warps per CTA, optional
+// deterministic grid reduction (Epi::K > 0) through the ticketed partials.
+template <class Src, class Epi, bool Unit>
+__global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, Src src_p, Epi epi_p) {
+    __shared__ double win[kGrpWarps][kGrpRound];
+    Epi epi = epi_p;
+    if (!epi.gate()) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) epi.off();
+        return;
+    }
+    Src src = src_p;
+    src.init();
+    const int nu = G.units();
+    for (int u = blockIdx.x * kGrpWarps + (threadIdx.x >> 5); u < nu; u += gridDim.x * kGrpWarps)
+        grp_unit<Unit>(A, G, u, src, epi, win[threadIdx.x >> 5]);
+    if constexpr (Epi::K > 0) {
+        double v[Epi::K];
+        epi.vals(v);
+        grid_reduce_finish<Epi::K>(v, epi.red.partials, epi.red.ticket,
+                                                   [&](const double (&t)[Epi::K]) { epi.fin(t); });
+    }
+}
+
+}  // namespace uaamg

@@ -1,8 +1,52 @@
 // kernels.h -- host-side launchers for the device kernels (internal).
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace uaamg {
+
+// Warp work units of one CSR operand (csr_group.cuh): row groups of 32
+// rows, plus pieces of rows longer than long_min (solve path only).
+struct Groups {
+    int n = 0;                   // rows
+    int ng = 0;                  // ceil(n / 32)
+    int np = 0;                  // long-row pieces
+    int long_min = 0x7fffffff;   // rows longer than this are split into pieces
+    const int4* piece = nullptr; // {row, eb, ee, long-row id}
+    const int* pbase = nullptr;  // per long row: first partial slot (nlong + 1)
+    unsigned* ticket = nullptr;  // per long row, zero between uses
+    double* part = nullptr;      // np partial sums
+    __host__ __device__ int units() const { return ng + np; }
+};
+// exact groups (no pieces): every row folded sequentially in reference order
+inline Groups exact_groups(int n) {
+    Groups g;
+    g.n = n;
+    g.ng = (n + 31) / 32;
+    return g;
+}
+// owning storage for a Groups with pieces
+struct GroupBuf {
+    DBuf<int4> piece;
+    DBuf<int> pbase;
+    DBuf<unsigned> ticket;
+    DBuf<double> part;
+    Groups g;
+};
+// long_min: rows with more entries become pieces (solve path)
+void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s);
+constexpr int kSolveLongMin = 1024;
+
+struct Op;  // one recorded engine phase (ops.cuh)
+
+// Where a solve operation goes: launched on a stream, or -- rec != nullptr --
+// appended to an op list the persistent engine interprets (engine.cu).
+struct Exec {
+    cudaStream_t s = 0;
+    std::vector<Op>* rec = nullptr;
+    Exec(cudaStream_t st = 0, std::vector<Op>* r = nullptr) : s(st), rec(r) {}
+};
 
 constexpr int kMaxInner = 16;
 
@@ -41,54 +85,54 @@ constexpr int kMaxRedBlocks = 1 << 16;
 
 // ---- staged CSR operations (csr_stream.cuh) ----
 // kernel-table (bit-exact for every row length) variants
-void launch_spmv(const Csr& A, const Blocks& B, const double* x, double* y, cudaStream_t s);
-void launch_sweep_exact(const Csr& A, const Blocks& B, const double* invm, const double* b, const double* x,
+void launch_spmv(const Csr& A, const Groups& G, const double* x, double* y, cudaStream_t s);
+void launch_sweep_exact(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
                         double* out, cudaStream_t s);
-void launch_restrict_exact(int nc, const int* agg_ptr, const int* members, const Blocks& MB, const double* r,
+void launch_restrict_exact(int nc, const int* agg_ptr, const int* members, const Groups& MG, const double* r,
                            double* rc, cudaStream_t s);
 // r = b - A x, x given (xmode 2) or implicit one sweep from zero (xmode 1) or zero (xmode 0)
-void launch_residual(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,
-                     const double* x, double* r, const int* gate, cudaStream_t s);
+void launch_residual(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
+                     const double* x, double* r, const int* gate, Exec ex);
 // one Jacobi/l1 sweep: out = x + invm (b - A x), x from a vector
-void launch_sweep_vec(const Csr& A, const Blocks& B, const double* invm, const double* b, const double* x,
-                      double* out, const int* gate, cudaStream_t s);
+void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
+                      double* out, const int* gate, Exec ex);
 // prolongation fused into a sweep: x = xpre + ec[v2a] built on the fly
-void launch_sweep_up(const Csr& A, const Blocks& B, int xmode, const double* invm, const double* b,
+void launch_sweep_up(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
                      const double* xpre, const int* v2a, const double* ec, const int* ec_valid, double* out,
-                     const int* gate, cudaStream_t s);
+                     const int* gate, Exec ex);
 // restriction as a unit-valued staged row sum over members_csr
-void launch_restrict(int nc, const int* agg_ptr, const int* members, const Blocks& MB, const double* r,
-                     double* rc, const int* gate, cudaStream_t s);
+void launch_restrict(int nc, const int* agg_ptr, const int* members, const Groups& MG, const double* r,
+                     double* rc, const int* gate, Exec ex);
 // direction + SpMV + dots, FCG flavour: p = z (+ beta pprev), ap = A p, pap, pr -> alpha, upd[step]
-void launch_dir_fcg(const Csr& A, const Blocks& B, const double* z, const double* pprev, int have_prev,
+void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                     const double* r, double* p, double* ap, FcgState* st, int step, RedScratch rs,
-                    cudaStream_t s);
+                    Exec ex);
 // NPCG flavour (have_prev / breakdown handled on device)
-void launch_dir_npcg(const Csr& A, const Blocks& B, const double* z, const double* pprev, const double* r,
+void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);
 
 // ---- elementwise / reductions ----
 void launch_inv_diag(const Csr& A, int l1, double omega, double* invm, int* bad_row, cudaStream_t s);
-void launch_xpre1(int n, const double* invm, const double* b, double* x, const int* gate, cudaStream_t s);
+void launch_xpre1(int n, const double* invm, const double* b, double* x, const int* gate, Exec ex);
 void launch_prolongate(int n, int xmode, const double* invm, const double* b, const double* xpre, const int* v2a,
-                       const double* ec, const int* ec_valid, double* out, const int* gate, cudaStream_t s);
+                       const double* ec, const int* ec_valid, double* out, const int* gate, Exec ex);
 // ||b|| -> st->bnorm, gate[0] = parent && !(||b|| <= 1e-14 ||b||)
-void launch_fcg_begin(int n, const double* b, const int* parent_gate, FcgState* st, RedScratch rs, cudaStream_t s);
+void launch_fcg_begin(int n, const double* b, const int* parent_gate, FcgState* st, RedScratch rs, Exec ex);
 // beta = -(z.apprev)/(pprev.apprev) into *beta (gate: flag pointer)
 void launch_beta(int n, const double* z, const double* pprev, const double* apprev, double* beta, const int* gate,
-                 const int* gate2, RedScratch rs, cudaStream_t s);
+                 const int* gate2, RedScratch rs, Exec ex);
 // x (+)= alpha p, r_out = r_in - alpha ap, rnorm -> gate[step+1]
 void launch_fcg_update(int n, int step, double* x, const double* p, const double* r_in, double* r_out,
-                       const double* ap, FcgState* st, int singular, RedScratch rs, cudaStream_t s);
+                       const double* ap, FcgState* st, int singular, RedScratch rs, Exec ex);
 void launch_npcg_update(int n, double* x, const double* p, double* r, const double* ap, NpcgState* st,
                         double* history, int singular, RedScratch rs, cudaStream_t s);
 // singular helpers: v -= mean(v)   (U/solvers.py:112-113)
-void launch_project_mean(int n, double* v, double* sum_slot, const int* gate, RedScratch rs, cudaStream_t s);
+void launch_project_mean(int n, double* v, double* sum_slot, const int* gate, RedScratch rs, Exec ex);
 // compatibility check + projection into out (U/solvers.py:116-125); flags st_err on drift
 void launch_check_compatible(int n, const double* b, double* out, int* err_flag, double* sum_slot,
-                             const int* gate, int level, RedScratch rs, cudaStream_t s);
+                             const int* gate, int level, RedScratch rs, Exec ex);
 // dense coarsest solve x = Minv b
-void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, cudaStream_t s);
+void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, Exec ex);
 // ||v||_2 on device into *out (plain, ungated)
 void launch_norm(int n, const double* v, double* out, RedScratch rs, cudaStream_t s);
 // NPCG init: bnorm, history[0], active

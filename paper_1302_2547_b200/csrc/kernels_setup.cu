@@ -517,29 +517,6 @@ __global__ void k_seg_starts(int n, int nc, const int* sorted_keys, int* ptr) {
     }
 }
 
-// ============================================================ row blocks
-// Rows are cut into tiles of kRowsPerBlock; each tile is split greedily into
-// blocks whose nonzeros fit kStageCap (a row longer than kStageCap forms a
-// block of its own and takes the kernel's long-row path).
-__global__ void k_tile_blocks(int n, const int* rp, const int* tile_off, int* cnt, int* start) {
-    const int ntiles = (n + kRowsPerBlock - 1) / kRowsPerBlock;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
-        const int r0 = t * kRowsPerBlock, r1 = min(n, r0 + kRowsPerBlock);
-        int c = 0, rows = 0, nz = 0;
-        int pos = tile_off ? tile_off[t] : 0;
-        for (int i = r0; i < r1; ++i) {
-            const int len = rp[i + 1] - rp[i];
-            if (rows > 0 && nz + len > kStageCap) { ++c; rows = 0; nz = 0; }
-            if (rows == 0 && start) start[pos + c] = i;
-            nz += len;
-            ++rows;
-        }
-        if (rows > 0) ++c;
-        if (cnt) cnt[t] = c;
-    }
-}
-__global__ void k_block_end(int n, int nb, int* start) { start[nb] = n; }
-
 // ============================================================ Galerkin
 // stream length per aggregate: sum of its members' row lengths
 __global__ void k_stream_len(int nc, const int* agg_ptr, const int* members, const int* rp, int* slen) {
@@ -881,27 +858,6 @@ static void exclusive_scan(const T* in, T* out, int n, cudaStream_t s) {
     UA_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
     DBuf<char> t(tmp, s);
     UA_CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, s));
-}
-
-void build_row_blocks(int n, const int* rp, DBuf<int>& start, int& nb, cudaStream_t s) {
-    if (n == 0) {
-        nb = 0;
-        start.alloc(1, s);
-        UA_CK(cudaMemsetAsync(start.p, 0, sizeof(int), s));
-        return;
-    }
-    const int nt = (n + kRowsPerBlock - 1) / kRowsPerBlock;
-    DBuf<int> cnt(nt + 1, s), off(nt + 1, s);
-    UA_LAUNCH(k_tile_blocks, grid_for(nt), 256, 0, s, n, rp, (const int*)nullptr, cnt.p, (int*)nullptr);
-    UA_CK(cudaMemsetAsync(cnt.p + nt, 0, sizeof(int), s));
-    exclusive_scan(cnt.p, off.p, nt + 1, s);
-    int h_nb = 0;
-    UA_CK(cudaMemcpyAsync(&h_nb, off.p + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
-    UA_CK(cudaStreamSynchronize(s));
-    nb = h_nb;
-    start.alloc(nb + 1, s);
-    UA_LAUNCH(k_tile_blocks, grid_for(nt), 256, 0, s, n, rp, (const int*)off.p, (int*)nullptr, start.p);
-    UA_LAUNCH(k_block_end, 1, 1, 0, s, n, nb, start.p);
 }
 
 // aggregate() on device.  state arrays are n-sized scratch.

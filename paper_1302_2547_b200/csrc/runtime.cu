@@ -14,12 +14,16 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
+#include "engine.h"
 #include "setup.h"
 
 namespace uaamg {
@@ -31,18 +35,17 @@ struct Level {
     long long nnz = 0;
     DBuf<int> rp, ci;
     DBuf<double> av;
-    DBuf<int> blk;
-    int nb = 0;
+    GroupBuf grp;   // warp work units of A (solve path: long rows split)
     int nc = 0;  // 0 on the coarsest level
-    DBuf<int> v2a, seeds, agg_ptr, members, mblk;
-    int mnb = 0;
+    DBuf<int> v2a, seeds, agg_ptr, members;
+    GroupBuf mgrp;  // warp work units of members_csr (restriction)
     Csr csr() const {
         Csr c;
         c.n = n; c.nnz = (int)nnz; c.rp = rp.p; c.ci = ci.p; c.av = av.p;
         return c;
     }
-    Blocks blocks() const { return Blocks{nb, blk.p}; }
-    Blocks mblocks() const { return Blocks{mnb, mblk.p}; }
+    const Groups& groups() const { return grp.g; }
+    const Groups& mgroups() const { return mgrp.g; }
 };
 
 struct LevelWs {
@@ -63,6 +66,16 @@ struct SolveWs {
     DBuf<int> bad_row;
     // outer vectors
     DBuf<double> r, z, p0, p1, ap0, ap1, hist, bproj;
+    // persistent coarse engine: levels >= Lc (Lc < 0: off)
+    int Lc = -1;
+    DBuf<Op> eops;
+    int neops = 0;
+    std::vector<Op> hops;                 // host copy of the op list (diagnostics)
+    DBuf<unsigned long long> eprof;       // UAAMG_ENGINE_PROF=1: op start times
+    std::vector<double> prof_acc;         // per-op accumulated seconds
+    int prof_runs = 0;
+    DBuf<double> epart;
+    DBuf<unsigned> ebar;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     uint64_t graph_kernels[2] = {0, 0};  // kernel launches recorded per graph
     // level-0 hot-kernel timing (profile_level0): event pairs per graph parity
@@ -156,7 +169,7 @@ static bool detect_singular(const Level& L, cudaStream_t s) {
     DBuf<unsigned long long> mx(2, s);
     UA_CK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
     UA_LAUNCH(k_fill, g1d(L.n), 256, 0, s, L.n, ones.p, 1.0);
-    launch_spmv(L.csr(), L.blocks(), ones.p, y.p, s);
+    launch_spmv(L.csr(), L.groups(), ones.p, y.p, s);
     UA_LAUNCH(k_maxabs_vals, g1d(L.nnz), 256, 0, s, (int)L.nnz, L.av.p, mx.p);
     UA_LAUNCH(k_maxabs_vals, g1d(L.n), 256, 0, s, L.n, y.p, mx.p + 1);
     unsigned long long h[2];
@@ -168,7 +181,7 @@ static bool detect_singular(const Level& L, cudaStream_t s) {
     return ax <= 1e-10 * scale;
 }
 
-static void finish_level(Level& L, cudaStream_t s) { build_row_blocks(L.n, L.rp.p, L.blk, L.nb, s); }
+static void finish_level(Level& L, cudaStream_t s) { build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s); }
 
 // aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)
 static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t s) {
@@ -245,7 +258,7 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         cur->agg_ptr.alloc(cur->nc + 1, s);
         cur->members.alloc(cur->n, s);
         build_members(cur->n, cur->nc, cur->v2a.p, cur->agg_ptr.p, cur->members.p, s);
-        build_row_blocks(cur->nc, cur->agg_ptr.p, cur->mblk, cur->mnb, s);
+        build_groups(cur->nc, cur->agg_ptr.p, kSolveLongMin, cur->mgrp, s);
         auto nxt = std::make_unique<Level>();
         nxt->n = cur->nc;
         nxt->nnz = device_galerkin(cur->csr(), cur->v2a.p, cur->nc, cur->agg_ptr.p, cur->members.p, nxt->rp, nxt->ci,
@@ -277,6 +290,8 @@ struct Plan {
     uaamg_solve_params p;
     cudaStream_t s;
     int prof = -1;  // >= 0: record level-0 timing events of this parity
+    std::vector<Op>* rec = nullptr;  // recording the engine's op list
+    Exec ex() const { return Exec(s, rec); }
     void mark(int k) {
         // External: a real event-record node inside the captured graph (a
         // plain cudaEventRecord during capture only orders nodes)
@@ -291,40 +306,45 @@ struct Plan {
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
         if (sing()) {
-            launch_check_compatible(L.n, b, W.bp.p, ws->err.p, ws->sums.p + 4 * l, gate, l, rs(), s);
+            launch_check_compatible(L.n, b, W.bp.p, ws->err.p, ws->sums.p + 4 * l, gate, l, rs(), ex());
             b = W.bp.p;
         }
         if (l == coarsest()) {
-            launch_dense_solve(L.n, h->Minv.p, b, out, gate, s);
-            if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 2, gate, rs(), s);
+            launch_dense_solve(L.n, h->Minv.p, b, out, gate, ex());
+            if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 2, gate, rs(), ex());
             return;
         }
         const Csr A = L.csr();
-        const Blocks B = L.blocks();
+        const Groups& B = L.groups();
         // pre-smoothing from a zero guess
         int xmode = p.pre_sweeps == 0 ? 0 : (p.pre_sweeps == 1 ? 1 : 2);
         const double* xpre = nullptr;
         double* cur = W.tA.p;
         if (xmode == 2) {
-            launch_xpre1(L.n, W.invm.p, b, W.tA.p, gate, s);
+            launch_xpre1(L.n, W.invm.p, b, W.tA.p, gate, ex());
             for (int k = 1; k < p.pre_sweeps; ++k) {
                 double* nx = (cur == W.tA.p) ? W.tB.p : W.tA.p;
-                launch_sweep_vec(A, B, W.invm.p, b, cur, nx, gate, s);
+                launch_sweep_vec(A, B, W.invm.p, b, cur, nx, gate, ex());
                 cur = nx;
             }
             xpre = cur;
         }
         // r = b - A x ; r_c = restrict(r)
         if (l == 0) mark(0);
-        launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, s);
+        launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, ex());
         if (l == 0) mark(1);
         LevelWs& C = ws->lev[l + 1];
-        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mblocks(), W.r.p, C.rhs.p, gate, s);
-        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), s);
+        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex());
+        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
         const bool exact = (l + 1 == coarsest());
         const double* ec;
         const int* ec_valid = nullptr;
-        if (!p.kcycle || p.inner_krylov_steps == 0 || exact) {
+        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
+        if (l + 1 == ws->Lc) {
+            engine(gate);
+            ec = direct ? C.e.p : C.xf.p;
+            if (!direct) ec_valid = &ws->fcg.p[l + 1].upd[0];
+        } else if (direct) {
             cycle(l + 1, C.rhs.p, C.e.p, gate);
             ec = C.e.p;
         } else {
@@ -334,21 +354,33 @@ struct Plan {
         }
         // prolongate + post-smoothing
         if (p.post_sweeps == 0) {
-            launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, s);
+            launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, ex());
         } else {
             double* other = (xpre == W.tA.p) ? W.tB.p : W.tA.p;
             double* dst = p.post_sweeps == 1 ? out : other;
             if (l == 0) mark(2);
-            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, s);
+            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex());
             if (l == 0) mark(3);
             double* c2 = dst;
             for (int k = 1; k < p.post_sweeps; ++k) {
                 double* nx = (k == p.post_sweeps - 1) ? out : ((c2 == W.tA.p) ? W.tB.p : W.tA.p);
-                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, s);
+                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, ex());
                 c2 = nx;
             }
         }
-        if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), s);
+        if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), ex());
+    }
+
+    // the whole recursion from level Lc down in one cooperative launch
+    void engine(const int* gate) {
+        EngineArgs a;
+        a.ops = ws->eops.p;
+        a.nops = ws->neops;
+        a.gate = gate;
+        a.partials = ws->epart.p;
+        a.bar = ws->ebar.p;
+        a.prof = ws->eprof.p;
+        launch_engine(a, s);
     }
 
     // U/solvers.py:160-187
@@ -356,7 +388,7 @@ struct Plan {
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
         FcgState* st = ws->fcg.p + l;
-        launch_fcg_begin(L.n, b, parent_gate, st, rs(), s);
+        launch_fcg_begin(L.n, b, parent_gate, st, rs(), ex());
         double* P[2] = {W.p0.p, W.p1.p};
         double* AP[2] = {W.ap0.p, W.ap1.p};
         for (int k = 0; k < p.inner_krylov_steps; ++k) {
@@ -367,9 +399,9 @@ struct Plan {
             double* pp = P[(k + 1) & 1];
             double* apc = AP[k & 1];
             double* app = AP[(k + 1) & 1];
-            if (k > 0) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), s);
-            launch_dir_fcg(L.csr(), L.blocks(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), s);
-            launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), s);
+            if (k > 0) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
+            launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
+            launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
         }
     }
 
@@ -388,7 +420,7 @@ struct Plan {
         if (sing()) launch_project_mean(L.n, ws->z.p, &st->sum, act, rs(), s);
         launch_beta(L.n, ws->z.p, pp, app, &st->beta, act, &st->have_prev, rs(), s);
         mark(4);
-        launch_dir_npcg(L.csr(), L.blocks(), ws->z.p, pp, ws->r.p, pc, apc, st, rs(), s);
+        launch_dir_npcg(L.csr(), L.groups(), ws->z.p, pp, ws->r.p, pc, apc, st, rs(), s);
         mark(5);
         launch_npcg_update(L.n, x, pc, ws->r.p, apc, st, ws->hist.p, sing(), rs(), s);
     }
@@ -399,7 +431,8 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
     const bool same = ws && ws->ready && ws->key.kcycle == p.kcycle &&
                       ws->key.inner_krylov_steps == p.inner_krylov_steps && ws->key.pre_sweeps == p.pre_sweeps &&
                       ws->key.post_sweeps == p.post_sweeps && ws->key.smoother_l1 == p.smoother_l1 &&
-                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters;
+                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters &&
+                      ws->key.engine_rows == p.engine_rows;
     if (same) return;
     if (ws) UA_CK(cudaStreamSynchronize(s));
     ws.reset(new SolveWs());
@@ -453,6 +486,44 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
     UA_CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     UA_CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
+    // persistent coarse engine from the first level (>= 1) small enough
+    const long long erows = p.engine_rows < 0 ? kEngDefaultRows : p.engine_rows;
+    ws->Lc = -1;
+    if (erows > 0)
+        for (int l = 1; l < nl; ++l)
+            if (h->levels[l]->n <= erows) { ws->Lc = l; break; }
+    if (ws->Lc > 0) {
+        // record cycle(Lc) / fcg(Lc) -- exactly what Plan::cycle(Lc - 1)
+        // would launch -- as the engine's op list
+        std::vector<Op> ops;
+        Plan rp{h, ws.get(), p, s};
+        rp.rec = &ops;
+        const int L0 = ws->Lc;
+        LevelWs& C = ws->lev[L0];
+        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || L0 == nl - 1;
+        if (direct) rp.cycle(L0, C.rhs.p, C.e.p, nullptr);
+        else rp.fcg(L0, C.rhs.p, C.xf.p, nullptr);
+        // schedule: small ops on one cluster; a grid barrier before the
+        // first big op after small ones
+        long long small_rows = kEngSmallRows;
+        if (const char* e = getenv("UAAMG_ENGINE_SMALL")) small_rows = atoll(e);
+        for (size_t k = 0; k < ops.size(); ++k) {
+            ops[k].small = ops[k].n <= small_rows ? 1 : 0;
+            ops[k].sync_before = (!ops[k].small && k > 0 && ops[k - 1].small) ? 1 : 0;
+        }
+        ws->neops = (int)ops.size();
+        ws->hops = ops;
+        if (getenv("UAAMG_ENGINE_PROF")) {
+            ws->eprof.alloc(ops.size() + 1, s);
+            ws->prof_acc.assign(ops.size(), 0.0);
+        }
+        ws->eops.alloc(std::max<size_t>(ops.size(), 1), s);
+        UA_CK(cudaMemcpyAsync(ws->eops.p, ops.data(), sizeof(Op) * ops.size(), cudaMemcpyHostToDevice, s));
+        ws->epart.alloc(4 * (size_t)kEngK * engine_grid(), s);
+        ws->ebar.alloc(2, s);
+        UA_CK(cudaMemsetAsync(ws->ebar.p, 0, 2 * sizeof(unsigned), s));
+        UA_CK(cudaStreamSynchronize(s));  // ops vector is a host temporary
+    }
     ws->ready = true;
     UA_CK(cudaStreamSynchronize(s));
 }
@@ -521,7 +592,7 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     if (x0) {
         UA_CK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         if (h->singular) launch_project_mean(n, x, ws->sums.p, nullptr, pl.rs(), s);
-        launch_spmv(L.csr(), L.blocks(), x, ws->z.p, s);
+        launch_spmv(L.csr(), L.groups(), x, ws->z.p, s);
         launch_axpby_init(n, bb, ws->z.p, ws->r.p, s);
     } else {
         UA_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
@@ -595,6 +666,21 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     UA_CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (ws->eprof.p && ws->neops > 0) {
+        // diagnostics: per-op durations of the last engine run, by (kind, rows)
+        std::vector<unsigned long long> t(ws->neops + 1);
+        UA_CK(cudaMemcpy(t.data(), ws->eprof.p, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+        std::map<std::pair<int, int>, std::pair<int, double>> agg;
+        for (int k = 0; k < ws->neops; ++k) {
+            auto& e = agg[{ws->hops[k].kind, ws->hops[k].n}];
+            e.first += 1;
+            e.second += (double)(t[k + 1] - t[k]) * 1e-3;
+        }
+        fprintf(stderr, "engine ops %d, total %.1f us\n", ws->neops, (double)(t[ws->neops] - t[0]) * 1e-3);
+        for (auto& kv : agg)
+            fprintf(stderr, "  kind %2d n %8d: %4d ops %9.1f us (%.2f us/op)\n", kv.first.first, kv.first.second,
+                    kv.second.first, kv.second.second, kv.second.second / kv.second.first);
+    }
     res->iterations = hst.iters;
     res->solve_seconds = ms * 1e-3;
     res->l0_kernel_launches = prof_n;
@@ -752,7 +838,7 @@ int uaamg_smooth(uaamg_hierarchy* h, const uaamg_solve_params* p, int level, con
             const double* cur = x;
             for (int k = 0; k < sweeps; ++k) {
                 double* nx = (k == sweeps - 1) ? out : ((cur == W.tA.p) ? W.tB.p : W.tA.p);
-                launch_sweep_vec(L.csr(), L.blocks(), W.invm.p, b, cur, nx, nullptr, s);
+                launch_sweep_vec(L.csr(), exact_groups(L.n), W.invm.p, b, cur, nx, nullptr, s);
                 cur = nx;
             }
         }

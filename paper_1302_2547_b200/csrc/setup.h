@@ -9,7 +9,6 @@ struct AggStats {
     int leftover = 0;
 };
 
-void build_row_blocks(int n, const int* rp, DBuf<int>& start, int& nb, cudaStream_t s);
 int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes, long long size_cap, int* v2a,
                      int* seeds, cudaStream_t s, AggStats* stats);
 void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cudaStream_t s);
