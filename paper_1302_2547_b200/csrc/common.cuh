@@ -35,6 +35,32 @@ extern std::atomic<uint64_t> g_launches;
         UA_CK(cudaGetLastError());                                               \
     } while (0)
 
+// Programmatic dependent launch (PDL): solve kernels are launched with
+// programmatic stream serialization, so a kernel's CTAs may start while its
+// predecessor drains.  Every such kernel calls pdl_wait() before touching
+// memory a predecessor wrote (griddepcontrol.wait returns once all
+// prerequisite grids completed and their writes are visible; a no-op when
+// launched without the attribute), and pdl_trigger() right after it to let
+// its own successor begin launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+#define UA_LAUNCH_PDL(kernel, grid, block, smem, strm, ...)                                   \
+    do {                                                                                        \
+        cudaLaunchConfig_t cfg_ = {};                                                           \
+        cfg_.gridDim = dim3(grid);                                                              \
+        cfg_.blockDim = dim3(block);                                                            \
+        cfg_.dynamicSmemBytes = (smem);                                                         \
+        cfg_.stream = (strm);                                                                   \
+        cudaLaunchAttribute at_[1];                                                             \
+        at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                         \
+        at_[0].val.programmaticStreamSerializationAllowed = 1;                                  \
+        cfg_.attrs = at_;                                                                       \
+        cfg_.numAttrs = 1;                                                                      \
+        UA_CK(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__));                                  \
+        ::uaamg::g_launches.fetch_add(1, std::memory_order_relaxed);                            \
+    } while (0)
+
 // ---------------------------------------------------------------- device memory
 // Stream-ordered allocation from the device's default memory pool.
 template <class T>
@@ -55,7 +81,9 @@ struct DBuf {
         release();
         s = st;
         n = count;
-        if (count) UA_CK(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+        // 64 bytes of tail slack: bulk (TMA) copies round slices up to 16-byte
+        // granules and may read past the last element
+        if (count) UA_CK(cudaMallocAsync((void**)&p, count * sizeof(T) + 64, st));
     }
     void release() {
         if (p) cudaFreeAsync(p, s);
@@ -112,13 +140,13 @@ __device__ __forceinline__ double block_sum(double v, double* sm /* >= NT/32 + 1
 // to partials[k*nb + block]; the last block to arrive (atomic ticket) sums
 // the partials in block order and calls fin(tot) on thread 0, then rearms
 // the ticket.  Must be called by all threads of every block of the launch.
-template <int K, class F>
+template <int K, int NT = kThreads, class F>
 __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* partials, unsigned* ticket, F&& fin) {
-    __shared__ double sm[kThreads / 32 + 1];
+    __shared__ double sm[NT / 32 + 1];
     __shared__ bool last;
     double tot[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) tot[k] = block_sum<kThreads>(v[k], sm);
+    for (int k = 0; k < K; ++k) tot[k] = block_sum<NT>(v[k], sm);
     const int nb = gridDim.x;
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -132,8 +160,8 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* parti
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         double s = 0.0;
-        for (int b = threadIdx.x; b < nb; b += kThreads) s += __ldcg(partials + k * nb + b);
-        tot[k] = block_sum<kThreads>(s, sm);
+        for (int b = threadIdx.x; b < nb; b += NT) s += __ldcg(partials + k * nb + b);
+        tot[k] = block_sum<NT>(s, sm);
     }
     if (threadIdx.x == 0) {
         fin(tot);

@@ -122,6 +122,8 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
 template <class Src, class Epi, bool Unit>
 __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, Src src_p, Epi epi_p) {
     __shared__ double win[kGrpWarps][kGrpRound];
+    pdl_wait();
+    pdl_trigger();
     Epi epi = epi_p;
     if (!epi.gate()) {
         if (blockIdx.x == 0 && threadIdx.x == 0) epi.off();

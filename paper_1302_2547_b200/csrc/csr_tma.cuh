@@ -1,0 +1,210 @@
+// csr_tma.cuh -- TMA-pipelined CSR row kernel for the large (HBM-bound)
+// levels.
+//
+// Persistent CTAs of kTmaRows threads walk 128-row tiles.  Thread 0 streams
+// each tile's row_ptr / col / val slices into a kTmaStages-deep shared-memory
+// ring with cp.async.bulk (completion on an mbarrier), kTmaStages-1 tiles
+// ahead of the tile being computed, so the matrix stream (12 B per nonzero,
+// ~75% of the algorithmic bytes) is always in flight without holding
+// registers.  Per tile: every thread prefetches its row's epilogue operands
+// into L1, gathers src(col) for the tile's entries (batched, coalesced
+// shared-memory reads of col), writes the rounded products over the staged
+// values, and after a CTA barrier folds its own row sequentially in
+// ascending k from 0.0 -- bit-identical to the reference's row loops
+// (K/numba_backend.py:47-56, :297-310) -- then runs the epilogue.
+// Used when every tile's nonzeros fit the stage (cap <= kTmaMaxCap).
+#pragma once
+#include "solve_ops.cuh"
+
+namespace uaamg {
+
+constexpr int kTmaRows = 128;      // rows per tile = threads per CTA
+constexpr int kTmaStages = 3;
+constexpr int kTmaMaxCap = 2048;   // max nonzeros per tile on this path
+constexpr int kTmaBatch = 8;       // gathers in flight per thread
+
+struct TmaLayout {
+    int rp_off, ci_off, av_off, stage;
+};
+__host__ __device__ inline TmaLayout tma_layout(int cap) {
+    TmaLayout L;
+    L.rp_off = 0;
+    L.ci_off = ((kTmaRows + 8) * 4 + 127) & ~127;
+    L.av_off = L.ci_off + (((cap + 8) * 4 + 127) & ~127);
+    L.stage = L.av_off + (((cap + 4) * 8 + 127) & ~127);
+    return L;
+}
+inline size_t tma_smem_bytes(int cap) { return (size_t)kTmaStages * tma_layout(cap).stage + 16 * kTmaStages; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(m)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(m))
+        : "memory");
+}
+__device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
+
+template <class Src, class Epi, bool Unit>
+__global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap, Src src_p, Epi epi_p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    pdl_wait();
+    pdl_trigger();
+    Epi epi = epi_p;
+    if (!epi.gate()) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) epi.off();
+        return;
+    }
+    Src src = src_p;
+    src.init();
+    const TmaLayout Ly = tma_layout(cap);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kTmaStages * Ly.stage);
+    const int t = threadIdx.x;
+    const int G = gridDim.x;
+    // tiles of this CTA: blockIdx.x + j * G
+    const int my = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
+    if (t == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&mbar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // producer (thread 0): issue tile j into stage j % kTmaStages
+    auto issue = [&](int j, int e0, int e1) {
+        const int tile = blockIdx.x + j * G;
+        const int s = j % kTmaStages;
+        unsigned char* st = smem + s * Ly.stage;
+        const int r0 = tile * kTmaRows, r1 = min(r0 + kTmaRows, A.n);
+        const unsigned brp = round16((unsigned)(r1 - r0 + 1) * 4u);
+        const int ea = e0 & ~3, eb = e0 & ~1;
+        const unsigned bci = round16((unsigned)(e1 - ea) * 4u);
+        const unsigned bav = Unit ? 0u : round16((unsigned)(e1 - eb) * 8u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[s], brp + bci + bav);
+        bulk_g2s(st + Ly.rp_off, A.rp + r0, brp, &mbar[s]);
+        if (bci) bulk_g2s(st + Ly.ci_off, A.ci + ea, bci, &mbar[s]);
+        if (bav) bulk_g2s(st + Ly.av_off, A.av + eb, bav, &mbar[s]);
+    };
+    auto bounds = [&](int j, int& e0, int& e1) {
+        const int r0 = (blockIdx.x + j * G) * kTmaRows;
+        e0 = __ldg(A.rp + r0);
+        e1 = __ldg(A.rp + min(r0 + kTmaRows, A.n));
+    };
+    int ne0 = 0, ne1 = 0;  // producer: bounds of the next tile to issue
+    if (my > 0 && blockIdx.x * kTmaRows + t < A.n) {
+        epi.pre(blockIdx.x * kTmaRows + t);
+        src.pre(blockIdx.x * kTmaRows + t);
+    }
+    if (t == 0) {
+        for (int j = 0; j < min(my, kTmaStages - 1); ++j) {
+            int e0, e1;
+            bounds(j, e0, e1);
+            issue(j, e0, e1);
+        }
+        if (kTmaStages - 1 < my) bounds(kTmaStages - 1, ne0, ne1);
+    }
+    // Software pipeline over this CTA's tiles: iteration j folds tile j
+    // (products already in its stage) while the gathers of tile j + 1 are
+    // in flight and tile j + 2 streams in by TMA.
+    double v[kTmaBatch];
+    int gb = 0, ge = 0, gea = 0;  // tile being gathered: entry range, col base
+    // gather phase 1: issue the loads of tile jj's first batch
+    auto gather_issue = [&](int jj) {
+        const int s = jj % kTmaStages;
+        const unsigned char* st = smem + s * Ly.stage;
+        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off);
+        const int* cis = reinterpret_cast<const int*>(st + Ly.ci_off);
+        mbar_wait(&mbar[s], (unsigned)((jj / kTmaStages) & 1));
+        const int r0 = (blockIdx.x + jj * G) * kTmaRows;
+        gb = rps[0];
+        ge = rps[min(kTmaRows, A.n - r0)];
+        gea = gb & ~3;
+#pragma unroll
+        for (int q = 0; q < kTmaBatch; ++q) {
+            const int e = gb + t + q * kTmaRows;
+            v[q] = e < ge ? src(cis[e - gea]) : 0.0;
+        }
+    };
+    // gather phase 2: products of tile jj into its stage (remaining batches
+    // are gathered and consumed directly)
+    auto gather_finish = [&](int jj) {
+        const int s = jj % kTmaStages;
+        unsigned char* st = smem + s * Ly.stage;
+        const int* cis = reinterpret_cast<const int*>(st + Ly.ci_off);
+        double* avs = reinterpret_cast<double*>(st + Ly.av_off);
+        const int eb = gb & ~1;
+        for (int base = gb + t;; base += kTmaRows * kTmaBatch) {
+#pragma unroll
+            for (int q = 0; q < kTmaBatch; ++q) {
+                const int e = base + q * kTmaRows;
+                if (e < ge) avs[e - eb] = Unit ? v[q] : __dmul_rn(avs[e - eb], v[q]);
+            }
+            const int nb = base + kTmaRows * kTmaBatch;
+            if (nb >= ge) break;
+#pragma unroll
+            for (int q = 0; q < kTmaBatch; ++q) {
+                const int e = nb + q * kTmaRows;
+                v[q] = e < ge ? src(cis[e - gea]) : 0.0;
+            }
+        }
+    };
+    if (my > 0) {
+        gather_issue(0);
+        gather_finish(0);
+    }
+    for (int j = 0; j < my; ++j) {
+        __syncthreads();  // products of tile j complete; stage of tile j - 1 free
+        // keep kTmaStages - 1 tiles in flight beyond the one being folded
+        if (t == 0 && j + kTmaStages - 1 < my) {
+            issue(j + kTmaStages - 1, ne0, ne1);
+            if (j + kTmaStages < my) bounds(j + kTmaStages, ne0, ne1);
+        }
+        const int s = j % kTmaStages;
+        const unsigned char* st = smem + s * Ly.stage;
+        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off);
+        const double* avs = reinterpret_cast<const double*>(st + Ly.av_off);
+        const int r0 = (blockIdx.x + j * G) * kTmaRows;
+        const int rows = min(kTmaRows, A.n - r0);
+        const int i = r0 + t;
+        const bool valid = t < rows;
+        if (j + 1 < my) {
+            // next tile's row operands and first gather batch go out now
+            const int i1 = r0 + G * kTmaRows + t;
+            if (i1 < A.n) {
+                epi.pre(i1);
+                src.pre(i1);
+            }
+            gather_issue(j + 1);
+        }
+        if (valid) {
+            const int eb = rps[0] & ~1;
+            const int b = rps[t] - eb, c = rps[t + 1] - eb;
+            double acc = 0.0;
+            for (int e = b; e < c; ++e) acc = __dadd_rn(acc, avs[e]);
+            epi.row(i, acc, src);
+        }
+        if (j + 1 < my) gather_finish(j + 1);
+    }
+    if constexpr (Epi::K > 0) {
+        double v[Epi::K];
+        epi.vals(v);
+        grid_reduce_finish<Epi::K, kTmaRows>(v, epi.red.partials, epi.red.ticket,
+                                             [&](const double (&tt)[Epi::K]) { epi.fin(tt); });
+    }
+}
+
+}  // namespace uaamg

@@ -17,6 +17,7 @@ struct Groups {
     const int* pbase = nullptr;  // per long row: first partial slot (nlong + 1)
     unsigned* ticket = nullptr;  // per long row, zero between uses
     double* part = nullptr;      // np partial sums
+    int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per 128-row tile
     __host__ __device__ int units() const { return ng + np; }
 };
 // exact groups (no pieces): every row folded sequentially in reference order
@@ -36,9 +37,21 @@ struct GroupBuf {
 };
 // long_min: rows with more entries become pieces (solve path)
 void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s);
-constexpr int kSolveLongMin = 1024;
+constexpr int kSolveLongMin = 256;
+// levels with at least this many rows take the TMA-pipelined tile kernel
+constexpr int kTmaMinRows = 65536;
+// max nonzeros over 128-row tiles (for the TMA path)
+int max_tile_nnz(int n, const int* rp, cudaStream_t s);
 
 struct Op;  // one recorded engine phase (ops.cuh)
+
+// fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
+struct BetaReq {
+    const double* apprev;
+    double* beta;
+    const double* pap;
+    const int* have;  // nullptr: always
+};
 
 // Where a solve operation goes: launched on a stream, or -- rec != nullptr --
 // appended to an op list the persistent engine interprets (engine.cu).
@@ -95,14 +108,15 @@ void launch_residual(const Csr& A, const Groups& G, int xmode, const double* inv
                      const double* x, double* r, const int* gate, Exec ex);
 // one Jacobi/l1 sweep: out = x + invm (b - A x), x from a vector
 void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
-                      double* out, const int* gate, Exec ex);
+                      double* out, const int* gate, Exec ex, const BetaReq* br = nullptr, RedScratch rs = {});
 // prolongation fused into a sweep: x = xpre + ec[v2a] built on the fly
 void launch_sweep_up(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
                      const double* xpre, const int* v2a, const double* ec, const int* ec_valid, double* out,
-                     const int* gate, Exec ex);
+                     const int* gate, Exec ex, const BetaReq* br = nullptr, RedScratch rs = {});
 // restriction as a unit-valued staged row sum over members_csr
+// begin_st: also start the coarse flexible CG (||r_c||, gate[0]) in the same kernel
 void launch_restrict(int nc, const int* agg_ptr, const int* members, const Groups& MG, const double* r,
-                     double* rc, const int* gate, Exec ex);
+                     double* rc, const int* gate, Exec ex, FcgState* begin_st = nullptr, RedScratch rs = {});
 // direction + SpMV + dots, FCG flavour: p = z (+ beta pprev), ap = A p, pap, pr -> alpha, upd[step]
 void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                     const double* r, double* p, double* ap, FcgState* st, int step, RedScratch rs,

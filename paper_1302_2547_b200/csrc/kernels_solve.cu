@@ -9,6 +9,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include "csr_group.cuh"
+#include "csr_tma.cuh"
 #include "ops.cuh"
 
 namespace uaamg {
@@ -22,8 +23,28 @@ static void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi&
         return;
     }
     if (G.units() == 0) return;
+    if (G.tma_cap > 0 && G.np == 0) {
+        // large level: TMA-pipelined persistent tiles
+        static int occ = -1, smem_set = 0;
+        const size_t smem = tma_smem_bytes(G.tma_cap);
+        auto kfn = k_csr_tma<Src, Epi, Unit>;
+        if ((int)smem > smem_set) {
+            UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set = (int)smem;
+            occ = -1;
+        }
+        static size_t occ_smem = 0;
+        if (occ < 0 || occ_smem != smem) {
+            UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem));
+            occ_smem = smem;
+        }
+        const int ntiles = cdiv(A.n, kTmaRows);
+        const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
+        UA_LAUNCH_PDL(kfn, grid, kTmaRows, smem, ex.s, A, ntiles, G.tma_cap, src, epi);
+        return;
+    }
     const int grid = std::min(cdiv(G.units(), kGrpWarps), kNumSMs * kGrpCtasPerSM);
-    UA_LAUNCH((k_csr_group<Src, Epi, Unit>), grid, 32 * kGrpWarps, 0, ex.s, A, G, src, epi);
+    UA_LAUNCH_PDL((k_csr_group<Src, Epi, Unit>), grid, 32 * kGrpWarps, 0, ex.s, A, G, src, epi);
 }
 
 void launch_spmv(const Csr& A, const Groups& G, const double* x, double* y, cudaStream_t s) {
@@ -57,8 +78,21 @@ void launch_residual(const Csr& A, const Groups& G, int xmode, const double* inv
     else run_stream<SrcVec, EpiResid, false>(A, G, SrcVec{x}, e, ex);
 }
 
+static EpiSweepBeta sweep_beta(const double* invm, const double* b, double* out, const int* gate,
+                               const BetaReq& br, RedScratch rs) {
+    EpiSweepBeta e{};
+    e.invm = invm; e.b = b; e.out = out; e.g = gate;
+    e.apprev = br.apprev; e.beta = br.beta; e.pap = br.pap; e.have = br.have;
+    e.red = {rs.partials, rs.ticket};
+    return e;
+}
+
 void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
-                      double* out, const int* gate, Exec ex) {
+                      double* out, const int* gate, Exec ex, const BetaReq* br, RedScratch rs) {
+    if (br) {
+        run_stream<SrcVec, EpiSweepBeta, false>(A, G, SrcVec{x}, sweep_beta(invm, b, out, gate, *br, rs), ex);
+        return;
+    }
     EpiSweep e{};
     e.invm = invm; e.b = b; e.out = out; e.g = gate;
     run_stream<SrcVec, EpiSweep, false>(A, G, SrcVec{x}, e, ex);
@@ -66,19 +100,29 @@ void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const d
 
 void launch_sweep_up(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
                      const double* xpre, const int* v2a, const double* ec, const int* ec_valid, double* out,
-                     const int* gate, Exec ex) {
-    EpiSweep e{};
-    e.invm = invm; e.b = b; e.out = out; e.g = gate;
+                     const int* gate, Exec ex, const BetaReq* br, RedScratch rs) {
     SrcUp src{};
     src.mode = xmode; src.invm = invm; src.b = b; src.xpre = xpre; src.v2a = v2a; src.ec = ec;
     src.ec_valid = ec_valid;
+    if (br) {
+        run_stream<SrcUp, EpiSweepBeta, false>(A, G, src, sweep_beta(invm, b, out, gate, *br, rs), ex);
+        return;
+    }
+    EpiSweep e{};
+    e.invm = invm; e.b = b; e.out = out; e.g = gate;
     run_stream<SrcUp, EpiSweep, false>(A, G, src, e, ex);
 }
 
 void launch_restrict(int nc, const int* agg_ptr, const int* members, const Groups& MG, const double* r,
-                     double* rc, const int* gate, Exec ex) {
+                     double* rc, const int* gate, Exec ex, FcgState* begin_st, RedScratch rs) {
     Csr P;
     P.n = nc; P.rp = agg_ptr; P.ci = members; P.av = nullptr;
+    if (begin_st) {
+        EpiRestrictBegin e{};
+        e.y = rc; e.g = gate; e.st = begin_st; e.red = {rs.partials, rs.ticket};
+        run_stream<SrcVec, EpiRestrictBegin, true>(P, MG, SrcVec{r}, e, ex);
+        return;
+    }
     EpiStoreG e{};
     e.y = rc; e.g = gate;
     run_stream<SrcVec, EpiStoreG, true>(P, MG, SrcVec{r}, e, ex);
@@ -115,6 +159,25 @@ __global__ void k_row_bounds(int m, const int* rows, const int* rp, int2* out) {
         out[k] = make_int2(rp[rows[k]], rp[rows[k] + 1]);
 }
 }  // namespace
+
+__global__ void k_tile_nnz_max(int n, const int* rp, int* out) {
+    const int nt = (n + kTmaRows - 1) / kTmaRows;
+    int m = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
+        m = max(m, rp[min((t + 1) * kTmaRows, n)] - rp[t * kTmaRows]);
+    atomicMax(out, m);
+}
+
+int max_tile_nnz(int n, const int* rp, cudaStream_t s) {
+    if (n == 0) return 0;
+    DBuf<int> m(1, s);
+    UA_CK(cudaMemsetAsync(m.p, 0, sizeof(int), s));
+    UA_LAUNCH(k_tile_nnz_max, std::min(cdiv(cdiv(n, kTmaRows), 256), 4 * kNumSMs), 256, 0, s, n, rp, m.p);
+    int h = 0;
+    UA_CK(cudaMemcpyAsync(&h, m.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    return h;
+}
 
 void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s) {
     out.g = exact_groups(n);
@@ -163,6 +226,8 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
 // ============================================================ map-reduce
 template <class Body>
 __global__ void __launch_bounds__(kThreads) k_map(int n, Body body_p) {
+    pdl_wait();
+    pdl_trigger();
     Body body = body_p;
     if (!body.gate()) {
         if (blockIdx.x == 0 && threadIdx.x == 0) body.off();
@@ -188,7 +253,7 @@ static void run_map(int n, const Body& body, Exec ex) {
         record_map(*ex.rec, n, body);
         return;
     }
-    UA_LAUNCH((k_map<Body>), map_grid(n), kThreads, 0, ex.s, n, body);
+    UA_LAUNCH_PDL((k_map<Body>), map_grid(n), kThreads, 0, ex.s, n, body);
 }
 
 
@@ -321,6 +386,8 @@ void launch_check_compatible(int n, const double* b, double* out, int* err_flag,
 // ---- dense coarsest solve x = Minv b (warp per row)
 __global__ void k_dense_solve(int n, const double* __restrict__ M, const double* __restrict__ b, double* x,
                               const int* gate) {
+    pdl_wait();
+    pdl_trigger();
     if (gate && !*gate) return;
     const int lane = threadIdx.x & 31;
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -336,7 +403,7 @@ void launch_dense_solve(int n, const double* Minv, const double* b, double* x, c
         record_dense(*ex.rec, DenseArgs{Minv, b, x, gate, n});
         return;
     }
-    UA_LAUNCH(k_dense_solve, cdiv(n, 8), 256, 0, ex.s, n, Minv, b, x, gate);
+    UA_LAUNCH_PDL(k_dense_solve, cdiv(n, 8), 256, 0, ex.s, n, Minv, b, x, gate);
 }
 
 void launch_norm(int n, const double* v, double* out, RedScratch rs, cudaStream_t s) {

@@ -31,7 +31,10 @@ struct DenseArgs {
     X(4, SrcVec, EpiStoreG, true)             \
     X(5, SrcUp, EpiSweep, false)              \
     X(6, SrcVec, EpiSweep, false)             \
-    X(7, SrcDir, EpiDirFcg, false)
+    X(7, SrcDir, EpiDirFcg, false)            \
+    X(8, SrcUp, EpiSweepBeta, false)          \
+    X(9, SrcVec, EpiSweepBeta, false)         \
+    X(10, SrcVec, EpiRestrictBegin, true)
 //   X(kind, Body)
 #define UA_ENGINE_MAP_OPS(X) \
     X(20, BodyXpre1)         \

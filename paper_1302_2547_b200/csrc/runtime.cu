@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "csr_tma.cuh"
 #include "engine.h"
 #include "setup.h"
 
@@ -181,7 +182,14 @@ static bool detect_singular(const Level& L, cudaStream_t s) {
     return ax <= 1e-10 * scale;
 }
 
-static void finish_level(Level& L, cudaStream_t s) { build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s); }
+static void finish_level(Level& L, cudaStream_t s) {
+    build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s);
+    static const bool no_tma = getenv("UAAMG_NO_TMA") != nullptr;  // A/B diagnostics
+    if (!no_tma && L.n >= kTmaMinRows && L.grp.g.np == 0) {
+        const int cap = max_tile_nnz(L.n, L.rp.p, s);
+        if (cap <= kTmaMaxCap) L.grp.g.tma_cap = std::max(cap, 4);
+    }
+}
 
 // aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)
 static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t s) {
@@ -301,8 +309,9 @@ struct Plan {
     int coarsest() const { return (int)h->levels.size() - 1; }
     bool sing() const { return h->singular; }
 
-    // U/solvers.py:128-157
-    void cycle(int l, const double* b, double* out, const int* gate) {
+    // U/solvers.py:128-157.  br: fuse the beta dot of the flexible CG that
+    // consumes `out` into the last sweep; returns whether that happened.
+    bool cycle(int l, const double* b, double* out, const int* gate, const BetaReq* br = nullptr) {
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
         if (sing()) {
@@ -312,7 +321,7 @@ struct Plan {
         if (l == coarsest()) {
             launch_dense_solve(L.n, h->Minv.p, b, out, gate, ex());
             if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 2, gate, rs(), ex());
-            return;
+            return false;
         }
         const Csr A = L.csr();
         const Groups& B = L.groups();
@@ -334,12 +343,15 @@ struct Plan {
         launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, ex());
         if (l == 0) mark(1);
         LevelWs& C = ws->lev[l + 1];
-        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex());
-        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
         const bool exact = (l + 1 == coarsest());
+        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
+        // the coarse flexible CG's ||r_c|| / gate[0] come out of the restriction
+        const bool begun = !direct && !sing();
+        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex(),
+                        begun ? ws->fcg.p + l + 1 : nullptr, rs());
+        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
         const double* ec;
         const int* ec_valid = nullptr;
-        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
         if (l + 1 == ws->Lc) {
             engine(gate);
             ec = direct ? C.e.p : C.xf.p;
@@ -348,27 +360,31 @@ struct Plan {
             cycle(l + 1, C.rhs.p, C.e.p, gate);
             ec = C.e.p;
         } else {
-            fcg(l + 1, C.rhs.p, C.xf.p, gate);
+            fcg(l + 1, C.rhs.p, C.xf.p, gate, begun);
             ec = C.xf.p;
             ec_valid = &ws->fcg.p[l + 1].upd[0];
         }
-        // prolongate + post-smoothing
+        // prolongate + post-smoothing (the last sweep may carry the beta dot)
+        const BetaReq* fb = sing() ? nullptr : br;
         if (p.post_sweeps == 0) {
             launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, ex());
+            fb = nullptr;
         } else {
             double* other = (xpre == W.tA.p) ? W.tB.p : W.tA.p;
             double* dst = p.post_sweeps == 1 ? out : other;
             if (l == 0) mark(2);
-            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex());
+            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex(),
+                            p.post_sweeps == 1 ? fb : nullptr, rs());
             if (l == 0) mark(3);
             double* c2 = dst;
             for (int k = 1; k < p.post_sweeps; ++k) {
                 double* nx = (k == p.post_sweeps - 1) ? out : ((c2 == W.tA.p) ? W.tB.p : W.tA.p);
-                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, ex());
+                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, ex(), k == p.post_sweeps - 1 ? fb : nullptr, rs());
                 c2 = nx;
             }
         }
         if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), ex());
+        return fb != nullptr;
     }
 
     // the whole recursion from level Lc down in one cooperative launch
@@ -384,22 +400,24 @@ struct Plan {
     }
 
     // U/solvers.py:160-187
-    void fcg(int l, const double* b, double* x, const int* parent_gate) {
+    // begun: ||b|| / gate[0] were produced by the caller's restriction
+    void fcg(int l, const double* b, double* x, const int* parent_gate, bool begun = false) {
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
         FcgState* st = ws->fcg.p + l;
-        launch_fcg_begin(L.n, b, parent_gate, st, rs(), ex());
+        if (!begun) launch_fcg_begin(L.n, b, parent_gate, st, rs(), ex());
         double* P[2] = {W.p0.p, W.p1.p};
         double* AP[2] = {W.ap0.p, W.ap1.p};
         for (int k = 0; k < p.inner_krylov_steps; ++k) {
             const int* g = &st->gate[k];
             const double* rin = (k == 0) ? b : W.rf.p;
-            cycle(l, rin, W.z.p, g);
             double* pc = P[k & 1];
             double* pp = P[(k + 1) & 1];
             double* apc = AP[k & 1];
             double* app = AP[(k + 1) & 1];
-            if (k > 0) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
+            const BetaReq br{app, &st->beta, &st->pap, nullptr};
+            const bool fused = cycle(l, rin, W.z.p, g, k > 0 ? &br : nullptr);
+            if (k > 0 && !fused) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
             launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
             launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
         }
@@ -416,9 +434,10 @@ struct Plan {
         double* pp = P[parity ^ 1];
         double* apc = AP[parity];
         double* app = AP[parity ^ 1];
-        cycle(0, ws->r.p, ws->z.p, act);
+        const BetaReq br{app, &st->beta, &st->pap, &st->have_prev};
+        const bool fused = cycle(0, ws->r.p, ws->z.p, act, sing() ? nullptr : &br);
         if (sing()) launch_project_mean(L.n, ws->z.p, &st->sum, act, rs(), s);
-        launch_beta(L.n, ws->z.p, pp, app, &st->beta, act, &st->have_prev, rs(), s);
+        if (!fused) launch_beta(L.n, ws->z.p, pp, app, &st->beta, act, &st->have_prev, rs(), s);
         mark(4);
         launch_dir_npcg(L.csr(), L.groups(), ws->z.p, pp, ws->r.p, pc, apc, st, rs(), s);
         mark(5);
@@ -502,7 +521,7 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
         LevelWs& C = ws->lev[L0];
         const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || L0 == nl - 1;
         if (direct) rp.cycle(L0, C.rhs.p, C.e.p, nullptr);
-        else rp.fcg(L0, C.rhs.p, C.xf.p, nullptr);
+        else rp.fcg(L0, C.rhs.p, C.xf.p, nullptr, !h->singular);
         // schedule: small ops on one cluster; a grid barrier before the
         // first big op after small ones
         long long small_rows = kEngSmallRows;

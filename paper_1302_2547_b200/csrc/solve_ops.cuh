@@ -20,6 +20,9 @@ namespace uaamg {
 
 __device__ __forceinline__ double ldv(const double* p) { return *p; }
 __device__ __forceinline__ int ldv(const int* p) { return *p; }
+// L1 prefetch of a per-row operand (TMA path: issued before the gathers so
+// the epilogue's loads hit)
+__device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // Epilogue contract:
 //   __device__ void row(int i, double acc, const Src& src);   // per row
@@ -43,6 +46,7 @@ struct RedSlot {
 // x_k = 0 (no pre-smoothing: smooth(..., sweeps=0) returns the zero guess)
 struct SrcZero {
     __device__ void init() {}
+    __device__ void pre(int) const {}
     __device__ double operator()(int) const { return 0.0; }
 };
 
@@ -50,6 +54,7 @@ struct SrcZero {
 struct SrcVec {
     const double* x;
     __device__ void init() {}
+    __device__ void pre(int i) const { pf(x + i); }
     __device__ double operator()(int k) const { return ldv(x + k); }
 };
 
@@ -59,6 +64,7 @@ struct SrcPre1 {
     const double* invm;
     const double* b;
     __device__ void init() {}
+    __device__ void pre(int i) const { pf(invm + i); pf(b + i); }
     __device__ double operator()(int k) const { return __dadd_rn(0.0, __dmul_rn(ldv(invm + k), ldv(b + k))); }
 };
 
@@ -74,6 +80,11 @@ struct SrcUp {
     const int* ec_valid;  // nullptr: always valid
     bool valid;
     __device__ void init() { valid = (ec_valid == nullptr) || (*ec_valid != 0); }
+    __device__ void pre(int i) const {
+        if (mode == 1) { pf(invm + i); pf(b + i); }
+        if (mode == 2) pf(xpre + i);
+        pf(v2a + i);
+    }
     __device__ double operator()(int k) const {
         double xp = mode == 0 ? 0.0
                   : mode == 1 ? __dadd_rn(0.0, __dmul_rn(ldv(invm + k), ldv(b + k)))
@@ -97,6 +108,7 @@ struct SrcDir {
         have = have_p ? *have_p : have_static;
         beta = have ? *beta_p : 0.0;
     }
+    __device__ void pre(int i) const { pf(z + i); if (have) pf(pprev + i); }
     __device__ double operator()(int k) const {
         double zk = ldv(z + k);
         return have ? __dadd_rn(zk, __dmul_rn(beta, ldv(pprev + k))) : zk;
@@ -107,6 +119,7 @@ struct SrcDir {
 // ============================================================ epilogues
 struct EpiStore : NoReduce {
     double* y;
+    __device__ void pre(int) const {}
     __device__ bool gate() const { return true; }
     __device__ void off() {}
     template <class S>
@@ -118,6 +131,7 @@ struct EpiResid : NoReduce {
     const double* b;
     double* r;
     const int* g;
+    __device__ void pre(int i) const { pf(b + i); }
     __device__ bool gate() const { return g == nullptr || *g; }
     __device__ void off() {}
     template <class S>
@@ -130,12 +144,45 @@ struct EpiSweep : NoReduce {
     const double* b;
     double* out;
     const int* g;
+    __device__ void pre(int i) const { pf(invm + i); pf(b + i); }
     __device__ bool gate() const { return g == nullptr || *g; }
     __device__ void off() {}
     template <class S>
     __device__ void row(int i, double acc, const S& src) {
         const double r = __dsub_rn(b[i], acc);
         out[i] = __dadd_rn(src(i), __dmul_rn(invm[i], r));
+    }
+};
+
+// sweep + the dot of the flexible-CG beta that follows it (BodyBeta fused):
+// beta = -(z . ap_prev) / (p_prev . ap_prev), z = this sweep's output; the
+// denominator is the previous step's p'Ap -- the same dot of the same
+// vectors (U/solvers.py:175, :228).  have: nullptr = always.
+struct EpiSweepBeta {
+    static constexpr int K = 1;
+    const double* invm;
+    const double* b;
+    double* out;
+    const int* g;
+    const double* apprev;
+    double* beta;
+    const double* pap;
+    const int* have;
+    RedSlot<1> red;
+    double s0;
+    __device__ void pre(int i) const { pf(invm + i); pf(b + i); pf(apprev + i); }
+    __device__ bool gate() const { return g == nullptr || *g; }
+    __device__ void off() {}
+    template <class S>
+    __device__ void row(int i, double acc, const S& src) {
+        const double r = __dsub_rn(b[i], acc);
+        const double o = __dadd_rn(src(i), __dmul_rn(invm[i], r));
+        out[i] = o;
+        s0 += o * apprev[i];
+    }
+    __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void fin(const double (&t)[1]) {
+        if (have == nullptr || *have) *beta = -t[0] / *pap;
     }
 };
 
@@ -149,6 +196,7 @@ struct EpiDirFcg {
     int step;
     RedSlot<2> red;
     double s0, s1;
+    __device__ void pre(int i) const { pf(r + i); }
     __device__ bool gate() const { return st->gate[step] != 0; }
     __device__ void off() { st->upd[step] = 0; }
     template <class S>
@@ -178,6 +226,7 @@ struct EpiDirNpcg {
     NpcgState* st;
     RedSlot<2> red;
     double s0, s1;
+    __device__ void pre(int i) const { pf(r + i); }
     __device__ bool gate() const { return st->active != 0; }
     __device__ void off() {}
     template <class S>
@@ -207,10 +256,42 @@ struct EpiDirNpcg {
 struct EpiStoreG : NoReduce {
     double* y;
     const int* g;
+    __device__ void pre(int) const {}
     __device__ bool gate() const { return g == nullptr || *g; }
     __device__ void off() {}
     template <class S>
     __device__ void row(int i, double acc, const S&) { y[i] = acc; }
+};
+
+// restriction + the start of the coarse flexible CG (BodyFcgBegin fused):
+// ||r_c||, gate[0] (U/solvers.py:165, :169)
+struct EpiRestrictBegin {
+    static constexpr int K = 1;
+    double* y;
+    const int* g;
+    FcgState* st;
+    RedSlot<1> red;
+    double s0;
+    __device__ void pre(int) const {}
+    __device__ bool gate() const { return g == nullptr || *g; }
+    __device__ void off() {
+        st->gate[0] = 0;
+        st->upd[0] = 0;
+    }
+    template <class S>
+    __device__ void row(int i, double acc, const S&) {
+        y[i] = acc;
+        s0 += acc * acc;
+    }
+    __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void fin(const double (&t)[1]) {
+        const double nb = sqrt(t[0]);
+        st->bnorm = nb;
+        st->rnorm = nb;
+        st->gate[0] = (nb <= 1e-14 * nb) ? 0 : 1;
+        st->upd[0] = 0;
+        st->err = 0;
+    }
 };
 
 
