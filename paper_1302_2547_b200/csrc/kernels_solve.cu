@@ -16,6 +16,9 @@ namespace uaamg {
 
 std::atomic<uint64_t> g_launches{0};
 
+template <class Body>
+static void run_map(int n, const Body& body, Exec ex);
+
 template <class Src, class Epi, bool Unit>
 static void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
     if (ex.rec) {
@@ -135,6 +138,15 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.step = step; e.red = {rs.partials, rs.ticket};
     SrcDir src{};
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = nullptr; src.have_static = have_prev;
+    if (G.tma_cap > 0 && !ex.rec) {
+        // large level: p first, then a plain-gather SpMV (same arithmetic)
+        BodyDirP bp{};
+        bp.src = src; bp.p = p; bp.g = &st->gate[step];
+        run_map(A.n, bp, ex);
+        e.p = nullptr;
+        run_stream<SrcVec, EpiDirFcg, false>(A, G, SrcVec{p}, e, ex);
+        return;
+    }
     run_stream<SrcDir, EpiDirFcg, false>(A, G, src, e, ex);
 }
 
@@ -144,6 +156,14 @@ void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const doubl
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.red = {rs.partials, rs.ticket};
     SrcDir src{};
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = &st->have_prev;
+    if (G.tma_cap > 0) {
+        BodyDirP bp{};
+        bp.src = src; bp.p = p; bp.g = &st->active;
+        run_map(A.n, bp, s);
+        e.p = nullptr;
+        run_stream<SrcVec, EpiDirNpcg, false>(A, G, SrcVec{p}, e, s);
+        return;
+    }
     run_stream<SrcDir, EpiDirNpcg, false>(A, G, src, e, s);
 }
 

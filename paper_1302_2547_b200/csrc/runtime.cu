@@ -50,7 +50,7 @@ struct Level {
 };
 
 struct LevelWs {
-    DBuf<double> invm, r, rhs, e, tA, tB, bp;                // cycle
+    DBuf<double> invm, r, rhs, e, tA, tB, bp, xup;           // cycle (xup: large levels, post > 1)
     DBuf<double> xf, rf, z, p0, p1, ap0, ap1;                // inner FCG
 };
 
@@ -325,8 +325,13 @@ struct Plan {
         }
         const Csr A = L.csr();
         const Groups& B = L.groups();
-        // pre-smoothing from a zero guess
-        int xmode = p.pre_sweeps == 0 ? 0 : (p.pre_sweeps == 1 ? 1 : 2);
+        // pre-smoothing from a zero guess.  Large (HBM-bound) levels
+        // materialise the pre-smoothed iterate and the prolongated iterate
+        // instead of rebuilding them inside every gather: two cheap
+        // streaming passes make both SpMVs plain vector gathers (same
+        // arithmetic, same bits).
+        const bool mat = L.n >= kTmaMinRows;
+        int xmode = p.pre_sweeps == 0 ? 0 : (p.pre_sweeps == 1 && !mat ? 1 : 2);
         const double* xpre = nullptr;
         double* cur = W.tA.p;
         if (xmode == 2) {
@@ -372,10 +377,20 @@ struct Plan {
         } else {
             double* other = (xpre == W.tA.p) ? W.tB.p : W.tA.p;
             double* dst = p.post_sweeps == 1 ? out : other;
-            if (l == 0) mark(2);
-            launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex(),
-                            p.post_sweeps == 1 ? fb : nullptr, rs());
-            if (l == 0) mark(3);
+            if (mat) {
+                // x = xpre + e_c[v2a] into `other`, then a plain sweep
+                launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, other, gate, ex());
+                if (l == 0) mark(2);
+                launch_sweep_vec(A, B, W.invm.p, b, other, dst == other ? W.xup.p : dst, gate, ex(),
+                                 p.post_sweeps == 1 ? fb : nullptr, rs());
+                if (l == 0) mark(3);
+                if (dst == other) dst = W.xup.p;
+            } else {
+                if (l == 0) mark(2);
+                launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex(),
+                                p.post_sweeps == 1 ? fb : nullptr, rs());
+                if (l == 0) mark(3);
+            }
             double* c2 = dst;
             for (int k = 1; k < p.post_sweeps; ++k) {
                 double* nx = (k == p.post_sweeps - 1) ? out : ((c2 == W.tA.p) ? W.tB.p : W.tA.p);
@@ -481,6 +496,7 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
         W.r.alloc(n, s);
         W.tA.alloc(n, s);
         W.tB.alloc(n, s);
+        if (L.n >= kTmaMinRows && p.post_sweeps > 1) W.xup.alloc(n, s);
         if (l > 0 && p.kcycle && p.inner_krylov_steps > 0) {
             W.xf.alloc(n, s); W.rf.alloc(n, s); W.z.alloc(n, s);
             W.p0.alloc(n, s); W.p1.alloc(n, s); W.ap0.alloc(n, s); W.ap1.alloc(n, s);
@@ -815,8 +831,9 @@ int uaamg_solve_profile(const uaamg_hierarchy* h, double* seconds3, double* byte
         const double csr = 12.0 * nnz + 4.0 * (n + 1);
         // algorithmic bytes per launch ("Roofline"); x of the
         // one-sweep pre-smoother is rebuilt from b and inv_m on the fly
-        bytes3[0] = csr + 24.0 * n;             // residual: b, inv_m in; r out
-        bytes3[1] = csr + 28.0 * n + 8.0 * nc;  // up-sweep: b, inv_m, v2a, e_c in; x out
+        (void)nc;
+        bytes3[0] = csr + 24.0 * n;             // residual: x_pre (gathered), b in; r out
+        bytes3[1] = csr + 40.0 * n;             // post-sweep: x (gathered), b, inv_m, Ap_prev in; z out
         bytes3[2] = csr + 40.0 * n;             // direction SpMV: z, p_prev, r in; p, Ap out
         for (int k = 0; k < 3; ++k) seconds3[k] = h->ws->prof_seconds[k];
         *count = h->ws->prof_count;

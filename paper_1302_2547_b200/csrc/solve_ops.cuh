@@ -202,7 +202,7 @@ struct EpiDirFcg {
     template <class S>
     __device__ void row(int i, double acc, const S& src) {
         const double pi = src(i);
-        p[i] = pi;
+        if (p) p[i] = pi;  // nullptr: p was materialised before the SpMV
         ap[i] = acc;
         s0 += pi * acc;
         s1 += pi * r[i];
@@ -232,7 +232,7 @@ struct EpiDirNpcg {
     template <class S>
     __device__ void row(int i, double acc, const S& src) {
         const double pi = src(i);
-        p[i] = pi;
+        if (p) p[i] = pi;  // nullptr: p was materialised before the SpMV
         ap[i] = acc;
         s0 += pi * acc;
         s1 += pi * r[i];
@@ -299,6 +299,18 @@ struct BodyBase {
     __device__ bool gate() const { return true; }
     __device__ void off() {}
     __device__ void init() {}
+};
+
+// p = z + beta p_prev materialised ahead of the direction SpMV (large levels)
+struct BodyDirP {
+    static constexpr int K = 0;
+    SrcDir src;
+    double* p;
+    const int* g;
+    __device__ bool gate() const { return g == nullptr || *g; }
+    __device__ void off() {}
+    __device__ void init() { src.init(); }
+    __device__ void item(int i, double*) { p[i] = src(i); }
 };
 
 // ---- x = 0.0 + invm * b  (first sweep from a zero guess)
