@@ -193,6 +193,19 @@ typedef struct {
 int uaamg_npcg_solve(uaamg_hierarchy *h, const uaamg_solve_params *p, const double *b, const double *x0, double *x,
                      double *history_host, uaamg_solve_result *res, void *stream);
 
+/* U/solvers.py:190-255 as a ROW-PARTITIONED solve over `nranks` ranks
+ * (paper_1302_2547_b200/csrc/shard.cu): levels with at least
+ * shard_rows rows (level 0 always) are split into contiguous row ranges, one
+ * per rank; smaller levels are replicated.  Halo columns are gathered from
+ * the owning rank's buffer inside the SpMV and dot products are folded per
+ * rank, then across ranks in rank order.  This build runs the ranks as
+ * virtual ranks on the calling device (partition-invariance harness).  Same
+ * argument conventions as uaamg_npcg_solve; singular hierarchies are
+ * UAAMG_EUNSUPPORTED. */
+int uaamg_npcg_solve_sharded(uaamg_hierarchy *h, const uaamg_solve_params *p, int nranks, int64_t shard_rows,
+                             const double *b, const double *x0, double *x, double *history_host,
+                             uaamg_solve_result *res, void *stream);
+
 /* Level-0 hot-kernel timing of the last solve run with profile_level0 = 1:
  * device seconds summed over the working iterations (CUDA events captured
  * around the kernels inside the iteration graph) and algorithmic bytes per

@@ -80,6 +80,8 @@ _SIGS = {
     "uaamg_hierarchy_level": (_i, [_vp, _i, ctypes.POINTER(LevelView)]),
     "uaamg_npcg_solve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult),
                               _vp]),
+    "uaamg_npcg_solve_sharded": (_i, [_vp, ctypes.POINTER(SolveParams), _i, ctypes.c_int64, _vp, _vp, _vp, _vp,
+                                      ctypes.POINTER(SolveResult), _vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),
     "uaamg_smooth": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _i, _vp, _vp]),

@@ -42,9 +42,9 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
                                          double* win) {
     const int lane = threadIdx.x & 31;
     if (u < G.ng) {
-        const int i = (u << 5) + lane;
-        const int rlast = min((u << 5) + 32, G.n);
-        const bool valid = i < G.n;
+        const int i = G.base + (u << 5) + lane;
+        const int rlast = G.base + min((u << 5) + 32, G.n);
+        const bool valid = i < G.base + G.n;
         const int bi = valid ? __ldg(A.rp + i) : 0;
         const int ei = valid ? __ldg(A.rp + i + 1) : 0;
         const int e0 = __shfl_sync(0xffffffffu, bi, 0);
@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, S
     if constexpr (Epi::K > 0) {
         double v[Epi::K];
         epi.vals(v);
-        grid_reduce_finish<Epi::K>(v, epi.red.partials, epi.red.ticket,
-                                                   [&](const double (&t)[Epi::K]) { epi.fin(t); });
+        grid_reduce_finish<Epi::K>(v, epi.red.partials, epi.red.ticket, [&](const double (&t)[Epi::K]) {
+            if (!xpublish(epi.red, t)) epi.fin(t);
+        });
     }
 }
 

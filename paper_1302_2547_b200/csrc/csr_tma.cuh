@@ -61,7 +61,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
 
 template <class Src, class Epi, bool Unit>
-__global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap, Src src_p, Epi epi_p) {
+__global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, int ntiles, int cap, Src src_p, Epi epi_p) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_wait();
     pdl_trigger();
@@ -88,26 +88,27 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap
         const int tile = blockIdx.x + j * G;
         const int s = j % kTmaStages;
         unsigned char* st = smem + s * Ly.stage;
-        const int r0 = tile * kTmaRows, r1 = min(r0 + kTmaRows, A.n);
-        const unsigned brp = round16((unsigned)(r1 - r0 + 1) * 4u);
+        const int r0 = base + tile * kTmaRows, r1 = min(r0 + kTmaRows, end);
+        const int ra = r0 & ~3;  // 16-byte aligned row_ptr slice start
+        const unsigned brp = round16((unsigned)(r1 - ra + 1) * 4u);
         const int ea = e0 & ~3, eb = e0 & ~1;
         const unsigned bci = round16((unsigned)(e1 - ea) * 4u);
         const unsigned bav = Unit ? 0u : round16((unsigned)(e1 - eb) * 8u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&mbar[s], brp + bci + bav);
-        bulk_g2s(st + Ly.rp_off, A.rp + r0, brp, &mbar[s]);
+        bulk_g2s(st + Ly.rp_off, A.rp + ra, brp, &mbar[s]);
         if (bci) bulk_g2s(st + Ly.ci_off, A.ci + ea, bci, &mbar[s]);
         if (bav) bulk_g2s(st + Ly.av_off, A.av + eb, bav, &mbar[s]);
     };
     auto bounds = [&](int j, int& e0, int& e1) {
-        const int r0 = (blockIdx.x + j * G) * kTmaRows;
+        const int r0 = base + (blockIdx.x + j * G) * kTmaRows;
         e0 = __ldg(A.rp + r0);
-        e1 = __ldg(A.rp + min(r0 + kTmaRows, A.n));
+        e1 = __ldg(A.rp + min(r0 + kTmaRows, end));
     };
     int ne0 = 0, ne1 = 0;  // producer: bounds of the next tile to issue
-    if (my > 0 && blockIdx.x * kTmaRows + t < A.n) {
-        epi.pre(blockIdx.x * kTmaRows + t);
-        src.pre(blockIdx.x * kTmaRows + t);
+    if (my > 0 && base + blockIdx.x * kTmaRows + t < end) {
+        epi.pre(base + blockIdx.x * kTmaRows + t);
+        src.pre(base + blockIdx.x * kTmaRows + t);
     }
     if (t == 0) {
         for (int j = 0; j < min(my, kTmaStages - 1); ++j) {
@@ -126,12 +127,12 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap
     auto gather_issue = [&](int jj) {
         const int s = jj % kTmaStages;
         const unsigned char* st = smem + s * Ly.stage;
-        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off);
+        const int r0 = base + (blockIdx.x + jj * G) * kTmaRows;
+        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off) + (r0 & 3);
         const int* cis = reinterpret_cast<const int*>(st + Ly.ci_off);
         mbar_wait(&mbar[s], (unsigned)((jj / kTmaStages) & 1));
-        const int r0 = (blockIdx.x + jj * G) * kTmaRows;
         gb = rps[0];
-        ge = rps[min(kTmaRows, A.n - r0)];
+        ge = rps[min(kTmaRows, end - r0)];
         gea = gb & ~3;
 #pragma unroll
         for (int q = 0; q < kTmaBatch; ++q) {
@@ -175,16 +176,16 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap
         }
         const int s = j % kTmaStages;
         const unsigned char* st = smem + s * Ly.stage;
-        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off);
+        const int r0 = base + (blockIdx.x + j * G) * kTmaRows;
+        const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off) + (r0 & 3);
         const double* avs = reinterpret_cast<const double*>(st + Ly.av_off);
-        const int r0 = (blockIdx.x + j * G) * kTmaRows;
-        const int rows = min(kTmaRows, A.n - r0);
+        const int rows = min(kTmaRows, end - r0);
         const int i = r0 + t;
         const bool valid = t < rows;
         if (j + 1 < my) {
             // next tile's row operands and first gather batch go out now
             const int i1 = r0 + G * kTmaRows + t;
-            if (i1 < A.n) {
+            if (i1 < end) {
                 epi.pre(i1);
                 src.pre(i1);
             }
@@ -202,8 +203,9 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int ntiles, int cap
     if constexpr (Epi::K > 0) {
         double v[Epi::K];
         epi.vals(v);
-        grid_reduce_finish<Epi::K, kTmaRows>(v, epi.red.partials, epi.red.ticket,
-                                             [&](const double (&tt)[Epi::K]) { epi.fin(tt); });
+        grid_reduce_finish<Epi::K, kTmaRows>(v, epi.red.partials, epi.red.ticket, [&](const double (&tt)[Epi::K]) {
+            if (!xpublish(epi.red, tt)) epi.fin(tt);
+        });
     }
 }
 

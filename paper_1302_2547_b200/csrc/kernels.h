@@ -9,6 +9,7 @@ namespace uaamg {
 // Warp work units of one CSR operand (csr_group.cuh): row groups of 32
 // rows, plus pieces of rows longer than long_min (solve path only).
 struct Groups {
+    int base = 0;                // first row (a rank's row range [base, base + n))
     int n = 0;                   // rows
     int ng = 0;                  // ceil(n / 32)
     int np = 0;                  // long-row pieces
@@ -21,8 +22,9 @@ struct Groups {
     __host__ __device__ int units() const { return ng + np; }
 };
 // exact groups (no pieces): every row folded sequentially in reference order
-inline Groups exact_groups(int n) {
+inline Groups exact_groups(int n, int base = 0) {
     Groups g;
+    g.base = base;
     g.n = n;
     g.ng = (n + 31) / 32;
     return g;
@@ -36,12 +38,13 @@ struct GroupBuf {
     Groups g;
 };
 // long_min: rows with more entries become pieces (solve path)
-void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s);
+// rows [base, base + n) of a CSR with global row_ptr rp
+void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s, int base = 0);
 constexpr int kSolveLongMin = 256;
 // levels with at least this many rows take the TMA-pipelined tile kernel
 constexpr int kTmaMinRows = 65536;
 // max nonzeros over 128-row tiles (for the TMA path)
-int max_tile_nnz(int n, const int* rp, cudaStream_t s);
+int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0);
 
 struct Op;  // one recorded engine phase (ops.cuh)
 

@@ -8,47 +8,11 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
-#include "csr_group.cuh"
-#include "csr_tma.cuh"
-#include "ops.cuh"
+#include "launch.cuh"
 
 namespace uaamg {
 
 std::atomic<uint64_t> g_launches{0};
-
-template <class Body>
-static void run_map(int n, const Body& body, Exec ex);
-
-template <class Src, class Epi, bool Unit>
-static void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
-    if (ex.rec) {
-        record_csr<Src, Epi, Unit>(*ex.rec, A, G, src, epi);
-        return;
-    }
-    if (G.units() == 0) return;
-    if (G.tma_cap > 0 && G.np == 0) {
-        // large level: TMA-pipelined persistent tiles
-        static int occ = -1, smem_set = 0;
-        const size_t smem = tma_smem_bytes(G.tma_cap);
-        auto kfn = k_csr_tma<Src, Epi, Unit>;
-        if ((int)smem > smem_set) {
-            UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            smem_set = (int)smem;
-            occ = -1;
-        }
-        static size_t occ_smem = 0;
-        if (occ < 0 || occ_smem != smem) {
-            UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem));
-            occ_smem = smem;
-        }
-        const int ntiles = cdiv(A.n, kTmaRows);
-        const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
-        UA_LAUNCH_PDL(kfn, grid, kTmaRows, smem, ex.s, A, ntiles, G.tma_cap, src, epi);
-        return;
-    }
-    const int grid = std::min(cdiv(G.units(), kGrpWarps), kNumSMs * kGrpCtasPerSM);
-    UA_LAUNCH_PDL((k_csr_group<Src, Epi, Unit>), grid, 32 * kGrpWarps, 0, ex.s, A, G, src, epi);
-}
 
 void launch_spmv(const Csr& A, const Groups& G, const double* x, double* y, cudaStream_t s) {
     EpiStore e{};
@@ -180,7 +144,7 @@ __global__ void k_row_bounds(int m, const int* rows, const int* rp, int2* out) {
 }
 }  // namespace
 
-__global__ void k_tile_nnz_max(int n, const int* rp, int* out) {
+__global__ void k_tile_nnz_max(int n, const int* rp, int* out) {  // rp: first row of the range
     const int nt = (n + kTmaRows - 1) / kTmaRows;
     int m = 0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
@@ -188,7 +152,8 @@ __global__ void k_tile_nnz_max(int n, const int* rp, int* out) {
     atomicMax(out, m);
 }
 
-int max_tile_nnz(int n, const int* rp, cudaStream_t s) {
+int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base) {
+    rp += base;
     if (n == 0) return 0;
     DBuf<int> m(1, s);
     UA_CK(cudaMemsetAsync(m.p, 0, sizeof(int), s));
@@ -199,8 +164,9 @@ int max_tile_nnz(int n, const int* rp, cudaStream_t s) {
     return h;
 }
 
-void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s) {
-    out.g = exact_groups(n);
+void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s, int base) {
+    out.g = exact_groups(n, base);
+    rp += base;  // local view: row i of the range at rp[i]
     out.g.long_min = long_min;
     if (n == 0 || long_min == 0x7fffffff) return;
     DBuf<int> rows(n, s), cnt(1, s);
@@ -225,7 +191,7 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
     for (int k = 0; k < m; ++k) {
         pbase[k] = (int)pcs.size();
         for (int e = hb[k].x; e < hb[k].y; e += kGrpRound)
-            pcs.push_back(make_int4(hrows[k], e, std::min(e + kGrpRound, hb[k].y), k));
+            pcs.push_back(make_int4(base + hrows[k], e, std::min(e + kGrpRound, hb[k].y), k));
     }
     pbase[m] = (int)pcs.size();
     out.piece.alloc(pcs.size(), s);
@@ -242,40 +208,6 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
     out.g.ticket = out.ticket.p;
     out.g.part = out.part.p;
 }
-
-// ============================================================ map-reduce
-template <class Body>
-__global__ void __launch_bounds__(kThreads) k_map(int n, Body body_p) {
-    pdl_wait();
-    pdl_trigger();
-    Body body = body_p;
-    if (!body.gate()) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) body.off();
-        return;
-    }
-    body.init();
-    double v[Body::K > 0 ? Body::K : 1] = {};
-    for (int i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) body.item(i, v);
-    if constexpr (Body::K > 0) {
-        grid_reduce_finish<Body::K>(v, body.red.partials, body.red.ticket,
-                                    [&](const double (&t)[Body::K]) { body.fin(t); });
-    }
-}
-
-static int map_grid(int n) {
-    int g = cdiv(n, kThreads * 4);
-    return g < 1 ? 1 : (g > 2 * kNumSMs ? 2 * kNumSMs : g);
-}
-
-template <class Body>
-static void run_map(int n, const Body& body, Exec ex) {
-    if (ex.rec) {
-        record_map(*ex.rec, n, body);
-        return;
-    }
-    UA_LAUNCH_PDL((k_map<Body>), map_grid(n), kThreads, 0, ex.s, n, body);
-}
-
 
 // ---- smoother diagonal (U/solvers.py:69-81, K/numba_backend.py:59-84)
 __global__ void k_inv_diag(Csr A, int l1, double omega, double* invm, int* bad_row) {

@@ -1,0 +1,111 @@
+// launch.cuh -- host-side dispatch of the solve functors: run_stream (CSR
+// row operations: TMA tiles on large levels, warp groups otherwise, or an
+// engine op when recording) and run_map (elementwise + reductions), plus the
+// cross-rank reduction finish of the sharded solve (shard.cu).
+#pragma once
+#include "csr_group.cuh"
+#include "csr_tma.cuh"
+#include "ops.cuh"
+
+namespace uaamg {
+
+// ============================================================ map-reduce
+template <class Body>
+__global__ void __launch_bounds__(kThreads) k_map(int n, Body body_p) {
+    pdl_wait();
+    pdl_trigger();
+    Body body = body_p;
+    if (!body.gate()) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) body.off();
+        return;
+    }
+    body.init();
+    double v[Body::K > 0 ? Body::K : 1] = {};
+    for (int i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) body.item(i, v);
+    if constexpr (Body::K > 0) {
+        grid_reduce_finish<Body::K>(v, body.red.partials, body.red.ticket, [&](const double (&t)[Body::K]) {
+            if (!xpublish(body.red, t)) body.fin(t);
+        });
+    }
+}
+
+inline int map_grid(int n) {
+    int g = cdiv(n, kThreads * 4);
+    return g < 1 ? 1 : (g > 2 * kNumSMs ? 2 * kNumSMs : g);
+}
+
+template <class Body>
+void run_map(int n, const Body& body, Exec ex) {
+    if (ex.rec) {
+        record_map(*ex.rec, n, body);
+        return;
+    }
+    UA_LAUNCH_PDL((k_map<Body>), map_grid(n), kThreads, 0, ex.s, n, body);
+}
+
+
+
+template <class Body>
+void run_map(int n, const Body& body, Exec ex);
+
+template <class Src, class Epi, bool Unit>
+inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
+    if (ex.rec) {
+        record_csr<Src, Epi, Unit>(*ex.rec, A, G, src, epi);
+        return;
+    }
+    // an empty range still launches when it must publish a (zero) reduction
+    if (G.units() == 0) {
+        if constexpr (Epi::K == 0) return;
+        else if (epi.red.xslot == nullptr) return;
+    }
+    if (G.tma_cap > 0 && G.np == 0) {
+        // large level: TMA-pipelined persistent tiles
+        static int occ = -1, smem_set = 0;
+        const size_t smem = tma_smem_bytes(G.tma_cap);
+        auto kfn = k_csr_tma<Src, Epi, Unit>;
+        if ((int)smem > smem_set) {
+            UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set = (int)smem;
+            occ = -1;
+        }
+        static size_t occ_smem = 0;
+        if (occ < 0 || occ_smem != smem) {
+            UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem));
+            occ_smem = smem;
+        }
+        const int ntiles = cdiv(G.n, kTmaRows);
+        const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
+        UA_LAUNCH_PDL(kfn, grid, kTmaRows, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi);
+        return;
+    }
+    const int grid = std::min(cdiv(G.units(), kGrpWarps), kNumSMs * kGrpCtasPerSM);
+    UA_LAUNCH_PDL((k_csr_group<Src, Epi, Unit>), grid, 32 * kGrpWarps, 0, ex.s, A, G, src, epi);
+}
+
+
+// Sharded solve: the per-rank totals of a reduction were published into
+// every rank's slot array (xpublish); this folds them in rank order -- the
+// same bits on every rank -- and runs the op's fin() once.
+template <class T>
+__global__ void k_xfin(T obj, const double* slots, int P) {
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (!obj.gate()) return;  // the op was gated off: it published nothing and ran off()
+    double t[T::K];
+#pragma unroll
+    for (int k = 0; k < T::K; ++k) {
+        double s = 0.0;
+        for (int q = 0; q < P; ++q) s += __ldcg(slots + k * P + q);
+        t[k] = s;
+    }
+    obj.fin(t);
+}
+
+template <class T>
+void run_xfin(const T& obj, const double* slots, int P, cudaStream_t s) {
+    UA_LAUNCH_PDL((k_xfin<T>), 1, 32, 0, s, obj, slots, P);
+}
+
+}  // namespace uaamg

@@ -27,124 +27,11 @@
 #include "engine.h"
 #include "setup.h"
 
+#include "runtime.h"
+
 namespace uaamg {
 
 thread_local std::string g_last_error;
-
-struct Level {
-    int n = 0;
-    long long nnz = 0;
-    DBuf<int> rp, ci;
-    DBuf<double> av;
-    GroupBuf grp;   // warp work units of A (solve path: long rows split)
-    int nc = 0;  // 0 on the coarsest level
-    DBuf<int> v2a, seeds, agg_ptr, members;
-    GroupBuf mgrp;  // warp work units of members_csr (restriction)
-    Csr csr() const {
-        Csr c;
-        c.n = n; c.nnz = (int)nnz; c.rp = rp.p; c.ci = ci.p; c.av = av.p;
-        return c;
-    }
-    const Groups& groups() const { return grp.g; }
-    const Groups& mgroups() const { return mgrp.g; }
-};
-
-struct LevelWs {
-    DBuf<double> invm, r, rhs, e, tA, tB, bp, xup;           // cycle (xup: large levels, post > 1)
-    DBuf<double> xf, rf, z, p0, p1, ap0, ap1;                // inner FCG
-};
-
-struct SolveWs {
-    uaamg_solve_params key{};
-    bool ready = false;
-    std::vector<LevelWs> lev;
-    DBuf<FcgState> fcg;     // one per level
-    DBuf<NpcgState> npcg;
-    DBuf<double> partials;
-    DBuf<unsigned> ticket;
-    DBuf<double> sums;      // per-level scratch sums (singular)
-    DBuf<int> err;          // incompatibility flag
-    DBuf<int> bad_row;
-    // outer vectors
-    DBuf<double> r, z, p0, p1, ap0, ap1, hist, bproj;
-    // persistent coarse engine: levels >= Lc (Lc < 0: off)
-    int Lc = -1;
-    DBuf<Op> eops;
-    int neops = 0;
-    std::vector<Op> hops;                 // host copy of the op list (diagnostics)
-    DBuf<unsigned long long> eprof;       // UAAMG_ENGINE_PROF=1: op start times
-    std::vector<double> prof_acc;         // per-op accumulated seconds
-    int prof_runs = 0;
-    DBuf<double> epart;
-    DBuf<unsigned> ebar;
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    uint64_t graph_kernels[2] = {0, 0};  // kernel launches recorded per graph
-    // level-0 hot-kernel timing (profile_level0): event pairs per graph parity
-    // around the residual, fused up-sweep and direction-SpMV kernels
-    cudaEvent_t pev[2][6] = {};
-    bool profiled = false;
-    double prof_seconds[3] = {0, 0, 0};  // residual, up-sweep, direction SpMV
-    int64_t prof_count = 0;
-    bool graphs_built = false;
-    double* graph_x = nullptr;  // graphs bake in the iterate pointer
-    int* h_flags = nullptr;  // pinned
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    ~SolveWs() {
-        for (auto& g : graph) if (g) cudaGraphExecDestroy(g);
-        for (auto& row : pev)
-            for (auto& e : row) if (e) cudaEventDestroy(e);
-        if (h_flags) cudaFreeHost(h_flags);
-        for (auto& e : ev) if (e) cudaEventDestroy(e);
-    }
-};
-
-}  // namespace uaamg
-
-struct uaamg_hierarchy {
-    std::vector<std::unique_ptr<uaamg::Level>> levels;
-    bool singular = false;
-    int coarse_mode = 0;
-    uaamg::DBuf<double> Minv;
-    double grid_complexity = 1, operator_complexity = 1, setup_seconds = 0;
-    cudaStream_t stream = 0;  // library-owned non-blocking stream (capturable)
-    std::unique_ptr<uaamg::SolveWs> ws;
-    std::mutex mu;
-    ~uaamg_hierarchy() {
-        ws.reset();
-        levels.clear();
-        Minv.release();
-        if (stream) {
-            cudaStreamSynchronize(stream);
-            cudaStreamDestroy(stream);
-        }
-    }
-};
-
-namespace uaamg {
-
-// ------------------------------------------------------------------ helpers
-// Orders the library's own stream after the caller's stream on entry and the
-// caller's stream after the library's on exit (the caller may pass the legacy
-// default stream, which cannot be graph-captured).
-struct StreamJoin {
-    cudaStream_t caller, own;
-    StreamJoin(cudaStream_t c, cudaStream_t o) : caller(c), own(o) {
-        if (c == o) return;
-        cudaEvent_t ev;
-        UA_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        UA_CK(cudaEventRecord(ev, c));
-        UA_CK(cudaStreamWaitEvent(o, ev, 0));
-        cudaEventDestroy(ev);
-    }
-    ~StreamJoin() {
-        if (caller == own) return;
-        cudaEvent_t ev;
-        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;
-        cudaEventRecord(ev, own);
-        cudaStreamWaitEvent(caller, ev, 0);
-        cudaEventDestroy(ev);
-    }
-};
 
 __global__ void k_maxabs_vals(int m, const double* v, unsigned long long* out) {
     double mx = 0.0;
@@ -292,184 +179,10 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
 }
 
 // ------------------------------------------------------------------ solve plan
-struct Plan {
-    uaamg_hierarchy* h;
-    SolveWs* ws;
-    uaamg_solve_params p;
-    cudaStream_t s;
-    int prof = -1;  // >= 0: record level-0 timing events of this parity
-    std::vector<Op>* rec = nullptr;  // recording the engine's op list
-    Exec ex() const { return Exec(s, rec); }
-    void mark(int k) {
-        // External: a real event-record node inside the captured graph (a
-        // plain cudaEventRecord during capture only orders nodes)
-        if (prof >= 0) UA_CK(cudaEventRecordWithFlags(ws->pev[prof][k], s, cudaEventRecordExternal));
-    }
-    RedScratch rs() const { return RedScratch{ws->partials.p, ws->ticket.p}; }
-    int coarsest() const { return (int)h->levels.size() - 1; }
-    bool sing() const { return h->singular; }
 
-    // U/solvers.py:128-157.  br: fuse the beta dot of the flexible CG that
-    // consumes `out` into the last sweep; returns whether that happened.
-    bool cycle(int l, const double* b, double* out, const int* gate, const BetaReq* br = nullptr) {
-        Level& L = *h->levels[l];
-        LevelWs& W = ws->lev[l];
-        if (sing()) {
-            launch_check_compatible(L.n, b, W.bp.p, ws->err.p, ws->sums.p + 4 * l, gate, l, rs(), ex());
-            b = W.bp.p;
-        }
-        if (l == coarsest()) {
-            launch_dense_solve(L.n, h->Minv.p, b, out, gate, ex());
-            if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 2, gate, rs(), ex());
-            return false;
-        }
-        const Csr A = L.csr();
-        const Groups& B = L.groups();
-        // pre-smoothing from a zero guess.  Large (HBM-bound) levels
-        // materialise the pre-smoothed iterate and the prolongated iterate
-        // instead of rebuilding them inside every gather: two cheap
-        // streaming passes make both SpMVs plain vector gathers (same
-        // arithmetic, same bits).
-        const bool mat = L.n >= kTmaMinRows;
-        int xmode = p.pre_sweeps == 0 ? 0 : (p.pre_sweeps == 1 && !mat ? 1 : 2);
-        const double* xpre = nullptr;
-        double* cur = W.tA.p;
-        if (xmode == 2) {
-            launch_xpre1(L.n, W.invm.p, b, W.tA.p, gate, ex());
-            for (int k = 1; k < p.pre_sweeps; ++k) {
-                double* nx = (cur == W.tA.p) ? W.tB.p : W.tA.p;
-                launch_sweep_vec(A, B, W.invm.p, b, cur, nx, gate, ex());
-                cur = nx;
-            }
-            xpre = cur;
-        }
-        // r = b - A x ; r_c = restrict(r)
-        if (l == 0) mark(0);
-        launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, ex());
-        if (l == 0) mark(1);
-        LevelWs& C = ws->lev[l + 1];
-        const bool exact = (l + 1 == coarsest());
-        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
-        // the coarse flexible CG's ||r_c|| / gate[0] come out of the restriction
-        const bool begun = !direct && !sing();
-        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex(),
-                        begun ? ws->fcg.p + l + 1 : nullptr, rs());
-        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
-        const double* ec;
-        const int* ec_valid = nullptr;
-        if (l + 1 == ws->Lc) {
-            engine(gate);
-            ec = direct ? C.e.p : C.xf.p;
-            if (!direct) ec_valid = &ws->fcg.p[l + 1].upd[0];
-        } else if (direct) {
-            cycle(l + 1, C.rhs.p, C.e.p, gate);
-            ec = C.e.p;
-        } else {
-            fcg(l + 1, C.rhs.p, C.xf.p, gate, begun);
-            ec = C.xf.p;
-            ec_valid = &ws->fcg.p[l + 1].upd[0];
-        }
-        // prolongate + post-smoothing (the last sweep may carry the beta dot)
-        const BetaReq* fb = sing() ? nullptr : br;
-        if (p.post_sweeps == 0) {
-            launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, ex());
-            fb = nullptr;
-        } else {
-            double* other = (xpre == W.tA.p) ? W.tB.p : W.tA.p;
-            double* dst = p.post_sweeps == 1 ? out : other;
-            if (mat) {
-                // x = xpre + e_c[v2a] into `other`, then a plain sweep
-                launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, other, gate, ex());
-                if (l == 0) mark(2);
-                launch_sweep_vec(A, B, W.invm.p, b, other, dst == other ? W.xup.p : dst, gate, ex(),
-                                 p.post_sweeps == 1 ? fb : nullptr, rs());
-                if (l == 0) mark(3);
-                if (dst == other) dst = W.xup.p;
-            } else {
-                if (l == 0) mark(2);
-                launch_sweep_up(A, B, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, dst, gate, ex(),
-                                p.post_sweeps == 1 ? fb : nullptr, rs());
-                if (l == 0) mark(3);
-            }
-            double* c2 = dst;
-            for (int k = 1; k < p.post_sweeps; ++k) {
-                double* nx = (k == p.post_sweeps - 1) ? out : ((c2 == W.tA.p) ? W.tB.p : W.tA.p);
-                launch_sweep_vec(A, B, W.invm.p, b, c2, nx, gate, ex(), k == p.post_sweeps - 1 ? fb : nullptr, rs());
-                c2 = nx;
-            }
-        }
-        if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), ex());
-        return fb != nullptr;
-    }
-
-    // the whole recursion from level Lc down in one cooperative launch
-    void engine(const int* gate) {
-        EngineArgs a;
-        a.ops = ws->eops.p;
-        a.nops = ws->neops;
-        a.gate = gate;
-        a.partials = ws->epart.p;
-        a.bar = ws->ebar.p;
-        a.prof = ws->eprof.p;
-        launch_engine(a, s);
-    }
-
-    // U/solvers.py:160-187
-    // begun: ||b|| / gate[0] were produced by the caller's restriction
-    void fcg(int l, const double* b, double* x, const int* parent_gate, bool begun = false) {
-        Level& L = *h->levels[l];
-        LevelWs& W = ws->lev[l];
-        FcgState* st = ws->fcg.p + l;
-        if (!begun) launch_fcg_begin(L.n, b, parent_gate, st, rs(), ex());
-        double* P[2] = {W.p0.p, W.p1.p};
-        double* AP[2] = {W.ap0.p, W.ap1.p};
-        for (int k = 0; k < p.inner_krylov_steps; ++k) {
-            const int* g = &st->gate[k];
-            const double* rin = (k == 0) ? b : W.rf.p;
-            double* pc = P[k & 1];
-            double* pp = P[(k + 1) & 1];
-            double* apc = AP[k & 1];
-            double* app = AP[(k + 1) & 1];
-            const BetaReq br{app, &st->beta, &st->pap, nullptr};
-            const bool fused = cycle(l, rin, W.z.p, g, k > 0 ? &br : nullptr);
-            if (k > 0 && !fused) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
-            launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
-            launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
-        }
-    }
-
-    // one NPCG iteration (U/solvers.py:221-254); parity selects p/p_prev roles
-    void npcg_iteration(double* x, int parity) {
-        Level& L = *h->levels[0];
-        NpcgState* st = ws->npcg.p;
-        const int* act = &st->active;
-        double* P[2] = {ws->p0.p, ws->p1.p};
-        double* AP[2] = {ws->ap0.p, ws->ap1.p};
-        double* pc = P[parity];
-        double* pp = P[parity ^ 1];
-        double* apc = AP[parity];
-        double* app = AP[parity ^ 1];
-        const BetaReq br{app, &st->beta, &st->pap, &st->have_prev};
-        const bool fused = cycle(0, ws->r.p, ws->z.p, act, sing() ? nullptr : &br);
-        if (sing()) launch_project_mean(L.n, ws->z.p, &st->sum, act, rs(), s);
-        if (!fused) launch_beta(L.n, ws->z.p, pp, app, &st->beta, act, &st->have_prev, rs(), s);
-        mark(4);
-        launch_dir_npcg(L.csr(), L.groups(), ws->z.p, pp, ws->r.p, pc, apc, st, rs(), s);
-        mark(5);
-        launch_npcg_update(L.n, x, pc, ws->r.p, apc, st, ws->hist.p, sing(), rs(), s);
-    }
-};
-
-static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s) {
-    auto& ws = h->ws;
-    const bool same = ws && ws->ready && ws->key.kcycle == p.kcycle &&
-                      ws->key.inner_krylov_steps == p.inner_krylov_steps && ws->key.pre_sweeps == p.pre_sweeps &&
-                      ws->key.post_sweeps == p.post_sweeps && ws->key.smoother_l1 == p.smoother_l1 &&
-                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters &&
-                      ws->key.engine_rows == p.engine_rows;
-    if (same) return;
-    if (ws) UA_CK(cudaStreamSynchronize(s));
-    ws.reset(new SolveWs());
+std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, bool engine,
+                                  int mat_levels) {
+    std::unique_ptr<SolveWs> ws(new SolveWs());
     ws->key = p;
     const int nl = (int)h->levels.size();
     ws->lev.resize(nl);
@@ -496,7 +209,7 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
         W.r.alloc(n, s);
         W.tA.alloc(n, s);
         W.tB.alloc(n, s);
-        if (L.n >= kTmaMinRows && p.post_sweeps > 1) W.xup.alloc(n, s);
+        if ((L.n >= kTmaMinRows || l < mat_levels) && p.post_sweeps > 1) W.xup.alloc(n, s);
         if (l > 0 && p.kcycle && p.inner_krylov_steps > 0) {
             W.xf.alloc(n, s); W.rf.alloc(n, s); W.z.alloc(n, s);
             W.p0.alloc(n, s); W.p1.alloc(n, s); W.ap0.alloc(n, s); W.ap1.alloc(n, s);
@@ -509,7 +222,6 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
         UA_CK(cudaMemcpyAsync(&h_bad, ws->bad_row.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         UA_CK(cudaStreamSynchronize(s));
         if (h_bad != 0x7fffffff) {
-            ws.reset();
             throw Error(UAAMG_ENUMERICAL, "non-positive smoother diagonal at row " + std::to_string(h_bad));
         }
     }
@@ -524,7 +236,7 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
     // persistent coarse engine from the first level (>= 1) small enough
     const long long erows = p.engine_rows < 0 ? kEngDefaultRows : p.engine_rows;
     ws->Lc = -1;
-    if (erows > 0)
+    if (engine && erows > 0)
         for (int l = 1; l < nl; ++l)
             if (h->levels[l]->n <= erows) { ws->Lc = l; break; }
     if (ws->Lc > 0) {
@@ -561,6 +273,20 @@ static void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStrea
     }
     ws->ready = true;
     UA_CK(cudaStreamSynchronize(s));
+    return ws;
+}
+
+void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s) {
+    auto& ws = h->ws;
+    const bool same = ws && ws->ready && ws->key.kcycle == p.kcycle &&
+                      ws->key.inner_krylov_steps == p.inner_krylov_steps && ws->key.pre_sweeps == p.pre_sweeps &&
+                      ws->key.post_sweeps == p.post_sweeps && ws->key.smoother_l1 == p.smoother_l1 &&
+                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters &&
+                      ws->key.engine_rows == p.engine_rows;
+    if (same) return;
+    if (ws) UA_CK(cudaStreamSynchronize(s));
+    ws.reset();
+    ws = build_ws(h, p, s, true, 0);
 }
 
 static void build_graphs(Plan& pl, double* x) {

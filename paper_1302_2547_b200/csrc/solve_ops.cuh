@@ -40,6 +40,35 @@ template <int K>
 struct RedSlot {
     double* partials;   // K * nb
     unsigned* ticket;   // zero between launches
+    // sharded solve: publish this rank's totals to every rank's slot array
+    // (xslot[q][k * xP + xrank]) instead of running fin(); k_xfin finishes
+    double* const* xslot = nullptr;
+    int xP = 0;
+    int xrank = 0;
+};
+
+template <int K>
+__device__ __forceinline__ bool xpublish(const RedSlot<K>& r, const double (&t)[K]) {
+    if (r.xslot == nullptr) return false;
+    for (int q = 0; q < r.xP; ++q)
+#pragma unroll
+        for (int k = 0; k < K; ++k) r.xslot[q][k * r.xP + r.xrank] = t[k];
+    __threadfence_system();
+    return true;
+}
+
+// ------------------------------------------------------------------ partitions
+// contiguous row ranges of a sharded level: rank q owns [b[q], b[q + 1])
+constexpr int kMaxRanks = 8;
+struct Part {
+    int P;
+    int b[kMaxRanks + 1];
+    __device__ __forceinline__ int owner(int k) const {
+        int q = 0;
+#pragma unroll
+        for (int j = 1; j < kMaxRanks; ++j) q += (j < P && k >= b[j]) ? 1 : 0;
+        return q;
+    }
 };
 
 // ------------------------------------------------------------------ sources
@@ -56,6 +85,16 @@ struct SrcVec {
     __device__ void init() {}
     __device__ void pre(int i) const { pf(x + i); }
     __device__ double operator()(int k) const { return ldv(x + k); }
+};
+
+// x_k read from the rank that owns row k: a local load for owned columns, a
+// peer-memory load (NVLink on a multi-GPU box) for halo columns
+struct SrcPeer {
+    Part pt;
+    const double* tab[kMaxRanks];
+    __device__ void init() {}
+    __device__ void pre(int) const {}
+    __device__ double operator()(int k) const { return ldv(tab[pt.owner(k)] + k); }
 };
 
 // pre-smoothed iterate from a zero guess, one sweep: 0.0 + inv_m_k * b_k
@@ -299,6 +338,34 @@ struct BodyBase {
     __device__ bool gate() const { return true; }
     __device__ void off() {}
     __device__ void init() {}
+};
+
+// prolongation on a rank's own rows (pointers shifted to the range): the
+// coarse correction e_c[v2a_i] is read from the rank that owns aggregate
+// v2a_i (K/numba_backend.py:288-294)
+struct BodyProlPeer {
+    static constexpr int K = 0;
+    int mode;  // 0: xpre = 0, 2: vector
+    const double* xpre;
+    const int* v2a;
+    Part pt;
+    const double* ec[kMaxRanks];
+    const int* ec_valid;
+    double* out;
+    const int* g;
+    bool valid;
+    __device__ bool gate() const { return g == nullptr || *g; }
+    __device__ void off() {}
+    __device__ void init() { valid = (ec_valid == nullptr) || (*ec_valid != 0); }
+    __device__ void item(int i, double*) {
+        const double xp = mode == 0 ? 0.0 : xpre[i];
+        double e = 0.0;
+        if (valid) {
+            const int c = v2a[i];
+            e = ldv(ec[pt.owner(c)] + c);
+        }
+        out[i] = __dadd_rn(xp, e);
+    }
 };
 
 // p = z + beta p_prev materialised ahead of the direction SpMV (large levels)
