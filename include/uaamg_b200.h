@@ -206,6 +206,30 @@ int uaamg_npcg_solve_sharded(uaamg_hierarchy *h, const uaamg_solve_params *p, in
                              const double *b, const double *x0, double *x, double *history_host,
                              uaamg_solve_result *res, void *stream);
 
+/* Multi-process form of uaamg_npcg_solve_sharded: one process per GPU,
+ * rank `rank` of `nranks`, each with its own (bit-identical) hierarchy.
+ * create -> handle (64-byte CUDA IPC handle of this rank's shared-vector
+ * arena) -> exchange the handles (e.g. torch.distributed all_gather) ->
+ * connect (nranks handles, rank order) -> solve (collective: every rank
+ * calls it with the same b / x0) -> free.  Halo columns are read straight
+ * from the peers' arenas over NVLink inside the SpMV gathers; phases are
+ * separated by a device-side flag barrier; dots are folded in rank order. */
+typedef struct uaamg_dist uaamg_dist;
+int uaamg_dist_create(uaamg_hierarchy *h, const uaamg_solve_params *p, int rank, int nranks, int64_t shard_rows,
+                      uaamg_dist **out);
+int uaamg_dist_handle(uaamg_dist *d, void *handle64);
+int uaamg_dist_connect(uaamg_dist *d, const void *handles);
+int uaamg_dist_solve(uaamg_dist *d, const double *b, const double *x0, double *x, double *history_host,
+                     uaamg_solve_result *res, void *stream);
+void uaamg_dist_free(uaamg_dist *d);
+
+/* Row partitions used by the sharded solve (host-only helpers):
+ * level 0 in equal 128-row-aligned contiguous blocks; a coarse level by seed
+ * ownership (aggregates are numbered by ascending seed, so rank q owns the
+ * aggregates whose seed lies in its fine rows).  bounds: nranks + 1 ints. */
+int uaamg_partition_rows(int n, int nranks, int *bounds);
+int uaamg_partition_coarse(const int *seeds, int nc, const int *fine_bounds, int nranks, int *bounds);
+
 /* Level-0 hot-kernel timing of the last solve run with profile_level0 = 1:
  * device seconds summed over the working iterations (CUDA events captured
  * around the kernels inside the iteration graph) and algorithmic bytes per

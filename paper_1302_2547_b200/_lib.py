@@ -82,6 +82,13 @@ _SIGS = {
                               _vp]),
     "uaamg_npcg_solve_sharded": (_i, [_vp, ctypes.POINTER(SolveParams), _i, ctypes.c_int64, _vp, _vp, _vp, _vp,
                                       ctypes.POINTER(SolveResult), _vp]),
+    "uaamg_dist_create": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _i, ctypes.c_int64, _vp]),
+    "uaamg_dist_handle": (_i, [_vp, _vp]),
+    "uaamg_dist_connect": (_i, [_vp, _vp]),
+    "uaamg_dist_solve": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
+    "uaamg_dist_free": (None, [_vp]),
+    "uaamg_partition_rows": (_i, [_i, _i, _vp]),
+    "uaamg_partition_coarse": (_i, [_vp, _i, _vp, _i, _vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),
     "uaamg_smooth": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _i, _vp, _vp]),

@@ -68,14 +68,22 @@ struct DBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = 0;
+    bool view = false;  // non-owning (memory lives in an arena)
     DBuf() = default;
     DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), view(o.view) { o.p = nullptr; o.n = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; view = o.view; o.p = nullptr; o.n = 0; }
         return *this;
+    }
+    // re-point at arena memory (the previous allocation is freed)
+    void adopt_view(T* ptr, size_t count) {
+        release();
+        p = ptr;
+        n = count;
+        view = true;
     }
     void alloc(size_t count, cudaStream_t st) {
         release();
@@ -86,9 +94,10 @@ struct DBuf {
         if (count) UA_CK(cudaMallocAsync((void**)&p, count * sizeof(T) + 64, st));
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p && !view) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
+        view = false;
     }
     ~DBuf() { release(); }
     T* get() const { return p; }

@@ -58,20 +58,47 @@ struct Sharded {
     uaamg_solve_params p;
     cudaStream_t s;
     int P;
-    int Ls = 0;  // first replicated level
-    std::vector<std::unique_ptr<SolveWs>> ws;
+    int rank = -1;          // -1: virtual ranks (all local); else this process's rank
+    std::vector<int> mine;  // ranks computed by this process
+    int Ls = 0;             // first replicated level
+    std::vector<std::unique_ptr<SolveWs>> ws;  // [rank] (null for remote ranks)
     std::vector<SLevel> lv;
     std::vector<DBuf<double>> xr, br;  // per rank: iterate and right-hand side
-    DBuf<double> slots;                // P x (kEngK * P)
-    DBuf<double*> slot_tab;            // P pointers into slots
+    DBuf<double> slots;                // virtual: P x (kEngK * P)
+    DBuf<double*> slot_tab;            // P pointers: slot array of every rank
+    // multi-process: every vector a peer may read lives in one cudaMalloc
+    // arena per rank (same layout everywhere), exported by CUDA IPC
+    char* arena = nullptr;
+    size_t arena_bytes = 0;
+    std::map<std::pair<int, int>, size_t> off;  // (level, role) -> arena offset
+    size_t slots_off = 0, flags_off = 0;
+    std::vector<char*> peer_base;               // arena base of every rank (own included)
+    DBuf<unsigned*> flag_tab;                   // P pointers: barrier flag array of every rank
+    unsigned epoch = 0;
+
+    ~Sharded() {
+        ws.clear();  // views into the arena go first
+        for (int q = 0; q < (int)peer_base.size(); ++q)
+            if (q != rank && peer_base[q]) cudaIpcCloseMemHandle(peer_base[q]);
+        if (arena) cudaFree(arena);
+    }
 
     Level& L(int l) const { return *h->levels[l]; }
     int a(int r, int l) const { return lv[l].part.b[r]; }
     int nrows(int r, int l) const { return lv[l].part.b[r + 1] - lv[l].part.b[r]; }
     RedScratch rs(int r) const { return RedScratch{ws[r]->partials.p, ws[r]->ticket.p}; }
-    const double* slot(int r) const { return slots.p + (size_t)r * kEngK * P; }
+    const double* slot(int r) const {
+        return rank < 0 ? slots.p + (size_t)r * kEngK * P : reinterpret_cast<const double*>(arena + slots_off);
+    }
+    // multi-process: cross-device barrier before an op reads what peers wrote
+    void sync();
 
     double* ptr(int r, VRef x) const {
+        if (rank >= 0 && r != rank) {
+            auto it = off.find({x.v >= T_R ? -1 : x.l, (int)x.v});
+            if (it == off.end()) throw Error(UAAMG_EINVAL, "vector is not shared across ranks");
+            return reinterpret_cast<double*>(peer_base[r] + it->second);
+        }
         SolveWs& W = *ws[r];
         switch (x.v) {
             case T_R: return W.r.p;
@@ -142,7 +169,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
     // pre-smoothing from a zero guess, materialised (x = 0 + inv_m b, then sweeps)
     VRef cur{l, V_TA};
     if (xmode == 2) {
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             BodyXpre1 body{};
             const int o = a(r, l);
             body.invm = ws[r]->lev[l].invm.p + o;
@@ -153,7 +181,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
         }
         for (int k = 1; k < p.pre_sweeps; ++k) {
             VRef nx{l, cur.v == V_TA ? V_TB : V_TA};
-            for (int r = 0; r < P; ++r) {
+            sync();
+            for (int r : mine) {
                 EpiSweep e{};
                 e.invm = ws[r]->lev[l].invm.p; e.b = ptr(r, b); e.out = ptr(r, nx); e.g = gptr(r, g);
                 run_stream<SrcPeer, EpiSweep, false>(A, lv[l].gA[r].g, peer(cur, l), e, s);
@@ -162,7 +191,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
         }
     }
     // r = b - A x
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         EpiResid e{};
         e.b = ptr(r, b); e.r = ptr(r, VRef{l, V_R}); e.g = gptr(r, g);
         if (xmode == 0) run_stream<SrcZero, EpiResid, false>(A, lv[l].gA[r].g, SrcZero{}, e, s);
@@ -176,7 +206,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
     const bool begun = !direct;
     Csr Pm;
     Pm.n = Lv.nc; Pm.rp = Lv.agg_ptr.p; Pm.ci = Lv.members.p; Pm.av = nullptr;
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         if (begun) {
             EpiRestrictBegin e{};
             e.y = ws[r]->lev[lc].rhs.p; e.g = gptr(r, g); e.st = fst(r, lc);
@@ -189,8 +220,9 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
             run_stream<SrcPeer, EpiStoreG, true>(Pm, lv[l].gP[r].g, peer(VRef{l, V_R}, l), e, s);
         }
     }
+    if (begun && csh) sync();
     if (begun && csh)
-        for (int r = 0; r < P; ++r) {
+        for (int r : mine) {
             EpiRestrictBegin e{};
             e.st = fst(r, lc);
             e.g = gptr(r, g);
@@ -202,7 +234,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
         if (direct) cycle(lc, VRef{lc, V_RHS}, ec, g, nullptr, 0);
         else fcg(lc, VRef{lc, V_RHS}, ec, g, true);
     } else {
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             Plan pl{h, ws[r].get(), p, s};
             LevelWs& C = ws[r]->lev[lc];
             if (direct) pl.cycle(lc, C.rhs.p, C.e.p, gptr(r, g));
@@ -211,7 +244,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
     }
     // prolongation on own rows into tB (or tA if the pre-iterate lives in tB)
     VRef other{l, cur.v == V_TA ? V_TB : V_TA};
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         const int o = a(r, l);
         BodyProlPeer body{};
         body.mode = xmode;
@@ -226,7 +260,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
     }
     // post-smoothing sweeps; the last may carry the consuming CG's beta dot
     if (p.post_sweeps == 0) {
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             const int o = a(r, l);
             UA_CK(cudaMemcpyAsync(ptr(r, out) + o, ptr(r, other) + o, sizeof(double) * nrows(r, l),
                                   cudaMemcpyDeviceToDevice, s));
@@ -237,7 +272,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
     for (int k = 0; k < p.post_sweeps; ++k) {
         const bool last = (k == p.post_sweeps - 1);
         VRef dst = last ? out : VRef{l, src.v == V_XUP ? V_TA : V_XUP};
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             if (last && apprev) {
                 EpiSweepBeta e{};
                 e.invm = ws[r]->lev[l].invm.p; e.b = ptr(r, b); e.out = ptr(r, dst); e.g = gptr(r, g);
@@ -258,8 +294,9 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
         }
         src = dst;
     }
+    if (apprev) sync();
     if (apprev)
-        for (int r = 0; r < P; ++r) {
+        for (int r : mine) {
             EpiSweepBeta e{};
             if (beta_state == 0) {
                 e.beta = &nst(r)->beta; e.pap = &nst(r)->pap; e.have = &nst(r)->have_prev;
@@ -275,7 +312,8 @@ bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int bet
 // U/solvers.py:160-187 on a sharded level (begun: ||b|| came from the restriction)
 void Sharded::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
     if (!begun) {
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             BodyFcgBegin body{};
             const int o = a(r, l);
             body.b = ptr(r, b) + o; body.pg = gptr(r, parent); body.st = fst(r, l);
@@ -283,7 +321,8 @@ void Sharded::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
             xred(body.red, r);
             run_map(nrows(r, l), body, s);
         }
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             BodyFcgBegin body{};
             body.st = fst(r, l);
             body.pg = gptr(r, parent);
@@ -298,7 +337,8 @@ void Sharded::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
         VRef pc{l, PR[k & 1]}, pp{l, PR[(k + 1) & 1]}, apc{l, APR[k & 1]}, app{l, APR[(k + 1) & 1]};
         cycle(l, rin, VRef{l, V_Z}, g, k > 0 ? &app : nullptr, 1);
         // p = z + beta p_prev on own rows, then Ap (+ p.Ap, p.r)
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             const int o = a(r, l);
             BodyDirP bp{};
             bp.src.z = ws[r]->lev[l].z.p + o; bp.src.pprev = ptr(r, pp) + o; bp.src.beta_p = &fst(r, l)->beta;
@@ -306,19 +346,22 @@ void Sharded::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
             bp.p = ptr(r, pc) + o; bp.g = gptr(r, g);
             run_map(nrows(r, l), bp, s);
         }
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             EpiDirFcg e{};
             e.p = nullptr; e.ap = ptr(r, apc); e.r = ptr(r, rin); e.st = fst(r, l); e.step = k;
             e.red = {rs(r).partials, rs(r).ticket};
             xred(e.red, r);
             run_stream<SrcPeer, EpiDirFcg, false>(A, lv[l].gA[r].g, peer(pc, l), e, s);
         }
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             EpiDirFcg e{};
             e.st = fst(r, l); e.step = k;
             run_xfin(e, slot(r), P, s);
         }
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             const int o = a(r, l);
             BodyFcgUpd body{};
             body.step = k; body.x = ptr(r, x) + o; body.p = ptr(r, pc) + o; body.rin = ptr(r, rin) + o;
@@ -327,7 +370,8 @@ void Sharded::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
             xred(body.red, r);
             run_map(nrows(r, l), body, s);
         }
-        for (int r = 0; r < P; ++r) {
+        sync();
+        for (int r : mine) {
             BodyFcgUpd body{};
             body.step = k; body.st = fst(r, l); body.singular = 0;
             run_xfin(body, slot(r), P, s);
@@ -342,7 +386,8 @@ void Sharded::npcg_iteration(int parity) {
     GRef act{1, 0, 0};
     cycle(0, VRef{0, T_R}, VRef{0, T_Z}, act, &app, 0);
     const Csr A = csr(0);
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         const int o = a(r, 0);
         BodyDirP bp{};
         bp.src.z = ws[r]->z.p + o; bp.src.pprev = ptr(r, pp) + o; bp.src.beta_p = &nst(r)->beta;
@@ -350,19 +395,22 @@ void Sharded::npcg_iteration(int parity) {
         bp.p = ptr(r, pc) + o; bp.g = gptr(r, act);
         run_map(nrows(r, 0), bp, s);
     }
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         EpiDirNpcg e{};
         e.p = nullptr; e.ap = ptr(r, apc); e.r = ws[r]->r.p; e.st = nst(r);
         e.red = {rs(r).partials, rs(r).ticket};
         xred(e.red, r);
         run_stream<SrcPeer, EpiDirNpcg, false>(A, lv[0].gA[r].g, peer(pc, 0), e, s);
     }
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         EpiDirNpcg e{};
         e.st = nst(r);
         run_xfin(e, slot(r), P, s);
     }
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         const int o = a(r, 0);
         BodyNpcgUpd body{};
         body.x = xr[r].p + o; body.p = ptr(r, pc) + o; body.r = ws[r]->r.p + o; body.ap = ptr(r, apc) + o;
@@ -371,7 +419,8 @@ void Sharded::npcg_iteration(int parity) {
         xred(body.red, r);
         run_map(nrows(r, 0), body, s);
     }
-    for (int r = 0; r < P; ++r) {
+    sync();
+    for (int r : mine) {
         BodyNpcgUpd body{};
         body.st = nst(r); body.hist = ws[r]->hist.p; body.singular = 0;
         run_xfin(body, slot(r), P, s);
@@ -397,21 +446,56 @@ Part level0_part(int n, int P) {
     return pt;
 }
 
-void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long long shard_rows, const double* b,
-                   const double* x0, double* x, double* hist_host, uaamg_solve_result* res, cudaStream_t s) {
+// aggregates are numbered by ascending seed: rank q's coarse rows are the
+// aggregates whose seed lies in its fine rows
+void coarse_part(const int* seeds, int nc, const int* fine, int P, int* out) {
+    for (int q = 0; q <= P; ++q) out[q] = (int)(std::lower_bound(seeds, seeds + nc, fine[q]) - seeds);
+    out[P] = nc;
+}
+
+// cross-device barrier: publish `epoch` into every rank's flag line, then
+// wait until every rank has published it into ours
+__global__ void k_dist_barrier(unsigned* const* flags, int P, int rank, unsigned epoch) {
+    __threadfence_system();  // this rank's earlier writes (own and peer) first
+    for (int q = 0; q < P; ++q) *(volatile unsigned*)(flags[q] + 32 * rank) = epoch;
+    __threadfence_system();
+    const volatile unsigned* mine = flags[rank];
+    const long long t0 = clock64();
+    for (int q = 0; q < P; ++q)
+        while ((int)(mine[32 * q] - epoch) < 0) {
+            __nanosleep(64);
+            if (clock64() - t0 > (1ll << 36)) __trap();  // a rank died: fail loudly
+        }
+    __threadfence_system();
+}
+
+void Sharded::sync() {
+    if (rank < 0) return;  // virtual ranks: stream order already orders the phases
+    ++epoch;
+    UA_LAUNCH(k_dist_barrier, 1, 1, 0, s, flag_tab.p, P, rank, epoch);
+}
+
+// partitions, workspaces, work-unit groups of the ranks this process runs
+std::unique_ptr<Sharded> sharded_build(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, int rank,
+                                       long long shard_rows, cudaStream_t s) {
     if (P < 1 || P > kMaxRanks) throw Error(UAAMG_EINVAL, "ranks must be in [1, 8]");
+    if (rank >= P) throw Error(UAAMG_EINVAL, "rank out of range");
     if (h->singular) throw Error(UAAMG_EUNSUPPORTED, "sharded solve of a singular (Neumann) hierarchy");
     if (!(p.tol > 0)) throw Error(UAAMG_EINVAL, "tol must be positive");
     const int nl = (int)h->levels.size();
-    Sharded S{h, p, s, P};
+    std::unique_ptr<Sharded> Sp(new Sharded{h, p, s, P});
+    Sharded& S = *Sp;
+    S.rank = rank;
+    if (rank < 0) for (int q = 0; q < P; ++q) S.mine.push_back(q);
+    else S.mine.push_back(rank);
     // sharded levels: level 0 always (when it has coarser levels), then every
     // level with >= shard_rows rows, never the coarsest
     S.Ls = 0;
     while (S.Ls < nl - 1 && (S.Ls == 0 || h->levels[S.Ls]->n >= shard_rows)) ++S.Ls;
     if (S.Ls == 0) throw Error(UAAMG_EUNSUPPORTED, "sharded solve needs at least two levels");
     S.lv.resize(nl);
-    for (int r = 0; r < P; ++r) S.ws.push_back(build_ws(h, p, s, false, S.Ls));
-    // partitions
+    S.ws.resize(P);
+    for (int r : S.mine) S.ws[r] = build_ws(h, p, s, false, S.Ls);
     S.lv[0].part = level0_part(h->levels[0]->n, P);
     for (int l = 0; l < S.Ls; ++l) {
         S.lv[l].sharded = true;
@@ -421,13 +505,11 @@ void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long 
         UA_CK(cudaStreamSynchronize(s));
         Part cp{};
         cp.P = P;
-        for (int q = 0; q <= P; ++q)
-            cp.b[q] = (int)(std::lower_bound(seeds.begin(), seeds.end(), S.lv[l].part.b[q]) - seeds.begin());
-        cp.b[P] = Lv.nc;
+        coarse_part(seeds.data(), Lv.nc, S.lv[l].part.b, P, cp.b);
         if (l + 1 < S.Ls) S.lv[l + 1].part = cp;
         S.lv[l].gA.resize(P);
         S.lv[l].gP.resize(P);
-        for (int r = 0; r < P; ++r) {
+        for (int r : S.mine) {
             const int a = S.lv[l].part.b[r], n = S.lv[l].part.b[r + 1] - a;
             build_groups(n, Lv.rp.p, kSolveLongMin, S.lv[l].gA[r], s, a);
             if (n >= kTmaMinRows / P && S.lv[l].gA[r].g.np == 0) {
@@ -441,38 +523,83 @@ void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long 
             build_groups(cn, Lv.agg_ptr.p, kSolveLongMin, S.lv[l].gP[r], s, ca);
         }
     }
-    // per-rank iterate / rhs, reduction slots
     const int n = h->levels[0]->n;
     S.xr.resize(P);
     S.br.resize(P);
-    for (int r = 0; r < P; ++r) {
+    for (int r : S.mine) {
         S.xr[r].alloc(n, s);
         S.br[r].alloc(n, s);
-        UA_CK(cudaMemcpyAsync(S.br[r].p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     }
-    S.slots.alloc((size_t)P * kEngK * P, s);
     S.slot_tab.alloc(P, s);
-    std::vector<double*> tab(P);
-    for (int r = 0; r < P; ++r) tab[r] = S.slots.p + (size_t)r * kEngK * P;
-    UA_CK(cudaMemcpyAsync(S.slot_tab.p, tab.data(), sizeof(double*) * P, cudaMemcpyHostToDevice, s));
+    if (rank < 0) {
+        S.slots.alloc((size_t)P * kEngK * P, s);
+        std::vector<double*> tab(P);
+        for (int q = 0; q < P; ++q) tab[q] = S.slots.p + (size_t)q * kEngK * P;
+        UA_CK(cudaMemcpyAsync(S.slot_tab.p, tab.data(), sizeof(double*) * P, cudaMemcpyHostToDevice, s));
+        UA_CK(cudaStreamSynchronize(s));
+        return Sp;
+    }
+    // multi-process: move every peer-readable vector into one arena
+    SolveWs& W = *S.ws[rank];
+    std::vector<std::pair<std::pair<int, int>, DBuf<double>*>> shared;
+    for (int l = 0; l < S.Ls; ++l) {
+        LevelWs& V = W.lev[l];
+        const std::pair<VRole, DBuf<double>*> roles[] = {{V_R, &V.r},   {V_TA, &V.tA},  {V_TB, &V.tB},
+                                                         {V_XUP, &V.xup}, {V_E, &V.e},  {V_XF, &V.xf},
+                                                         {V_P0, &V.p0}, {V_P1, &V.p1}};
+        for (auto& rb : roles)
+            if (rb.second->p) shared.push_back({{l, (int)rb.first}, rb.second});
+    }
+    shared.push_back({{-1, (int)T_P0}, &W.p0});
+    shared.push_back({{-1, (int)T_P1}, &W.p1});
+    shared.push_back({{-1, (int)T_X}, &S.xr[rank]});
+    size_t bytes = 0;
+    auto take = [&](size_t b) {
+        const size_t o = bytes;
+        bytes += (b + 64 + 255) & ~(size_t)255;
+        return o;
+    };
+    for (auto& e : shared) S.off[e.first] = take(e.second->n * sizeof(double));
+    S.slots_off = take(sizeof(double) * kEngK * P);
+    S.flags_off = take(sizeof(unsigned) * 32 * P);
+    S.arena_bytes = bytes;
+    UA_CK(cudaStreamSynchronize(s));
+    UA_CK(cudaMalloc(&S.arena, bytes));
+    UA_CK(cudaMemset(S.arena, 0, bytes));
+    for (auto& e : shared) e.second->adopt_view(reinterpret_cast<double*>(S.arena + S.off[e.first]), e.second->n);
+    return Sp;
+}
+
+// initial residual, the NPCG loop (U/solvers.py:202-255), x assembled from
+// the owners' slices
+void sharded_run(Sharded& S, const double* b, const double* x0, double* x, double* hist_host,
+                 uaamg_solve_result* res) {
+    uaamg_hierarchy* h = S.h;
+    const uaamg_solve_params& p = S.p;
+    cudaStream_t s = S.s;
+    const int P = S.P;
+    const int n = h->levels[0]->n;
+    const int me = S.mine[0];
+    for (int r : S.mine) UA_CK(cudaMemcpyAsync(S.br[r].p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     cudaEvent_t e0, e1;
     UA_CK(cudaEventCreate(&e0));
     UA_CK(cudaEventCreate(&e1));
     UA_CK(cudaEventRecord(e0, s));
-    // x, r initial (U/solvers.py:208-215)
     const Csr A = h->levels[0]->csr();
-    for (int r = 0; r < P; ++r) {
+    for (int r : S.mine) {
         if (x0) UA_CK(cudaMemcpyAsync(S.xr[r].p, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         else UA_CK(cudaMemsetAsync(S.xr[r].p, 0, sizeof(double) * n, s));
     }
-    for (int r = 0; r < P; ++r) {
+    S.sync();
+    for (int r : S.mine) {
         EpiResid e{};
         e.b = S.br[r].p; e.r = S.ws[r]->r.p; e.g = nullptr;
         if (x0) run_stream<SrcPeer, EpiResid, false>(A, S.lv[0].gA[r].g, S.peer(VRef{0, T_X}, 0), e, s);
         else run_stream<SrcZero, EpiResid, false>(A, S.lv[0].gA[r].g, SrcZero{}, e, s);
         UA_LAUNCH(k_set_npcg_sh, 1, 1, 0, s, S.nst(r), p.tol, p.max_iters);
     }
-    for (int r = 0; r < P; ++r) {
+    S.sync();
+    for (int r : S.mine) {
         const int o = S.a(r, 0);
         BodyNpcgInit body{};
         body.b = S.br[r].p + o; body.r = S.ws[r]->r.p + o; body.st = S.nst(r); body.hist = S.ws[r]->hist.p;
@@ -480,26 +607,30 @@ void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long 
         S.xred(body.red, r);
         run_map(S.nrows(r, 0), body, s);
     }
-    for (int r = 0; r < P; ++r) {
+    S.sync();
+    for (int r : S.mine) {
         BodyNpcgInit body{};
         body.st = S.nst(r); body.hist = S.ws[r]->hist.p;
         run_xfin(body, S.slot(r), P, s);
     }
     NpcgState hst{};
-    UA_CK(cudaMemcpyAsync(&hst, S.nst(0), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaMemcpyAsync(&hst, S.nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
     for (int it = 0; hst.active && it < p.max_iters; ++it) {
         S.npcg_iteration(it & 1);
-        UA_CK(cudaMemcpyAsync(&hst, S.nst(0), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaMemcpyAsync(&hst, S.nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
         UA_CK(cudaStreamSynchronize(s));
     }
     UA_CK(cudaEventRecord(e1, s));
-    // assemble x from the owners' slices
-    for (int r = 0; r < P; ++r) {
-        const int o = S.a(r, 0);
-        UA_CK(cudaMemcpyAsync(x + o, S.xr[r].p + o, sizeof(double) * S.nrows(r, 0), cudaMemcpyDeviceToDevice, s));
+    // assemble x from the owners' slices (peer reads in multi-process mode)
+    S.sync();
+    for (int q = 0; q < P; ++q) {
+        const int o = S.a(q, 0);
+        const double* src = S.rank < 0 || q == S.rank ? S.xr[q].p : S.ptr(q, VRef{0, T_X});
+        UA_CK(cudaMemcpyAsync(x + o, src + o, sizeof(double) * S.nrows(q, 0), cudaMemcpyDefault, s));
     }
-    UA_CK(cudaMemcpyAsync(&hst, S.nst(0), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+    S.sync();  // peers may not free their iterate before everyone copied it
+    UA_CK(cudaMemcpyAsync(&hst, S.nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
     float ms = 0;
     UA_CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -507,8 +638,8 @@ void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long 
     cudaEventDestroy(e1);
     res->iterations = hst.iters;
     res->solve_seconds = ms * 1e-3;
-    if (hist_host) UA_CK(cudaMemcpy(hist_host, S.ws[0]->hist.p, sizeof(double) * (hst.iters + 1),
-                                    cudaMemcpyDeviceToHost));
+    if (hist_host)
+        UA_CK(cudaMemcpy(hist_host, S.ws[me]->hist.p, sizeof(double) * (hst.iters + 1), cudaMemcpyDeviceToHost));
     res->converged = (hst.bnorm == 0.0) ? 1 : (hst.last_rel <= p.tol);
     res->status = 0;
     if (hst.status == 1) {
@@ -524,22 +655,120 @@ void sharded_solve(uaamg_hierarchy* h, const uaamg_solve_params& p, int P, long 
 
 using namespace uaamg;
 
-extern "C" int uaamg_npcg_solve_sharded(uaamg_hierarchy* h, const uaamg_solve_params* p, int nranks,
-                                        int64_t shard_rows, const double* b, const double* x0, double* x,
-                                        double* history_host, uaamg_solve_result* res, void* stream) {
-    try {
+struct uaamg_dist {
+    std::unique_ptr<uaamg::Sharded> S;
+};
+
+#define UA_TRY(...)                                                                                \
+    try {                                                                                          \
+        __VA_ARGS__;                                                                               \
+        const cudaError_t pe = cudaGetLastError();                                                 \
+        if (pe != cudaSuccess) throw Error(UAAMG_ECUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe)); \
+        return UAAMG_OK;                                                                           \
+    } catch (const Error& e) {                                                                     \
+        g_last_error = e.what();                                                                   \
+        return e.code;                                                                             \
+    } catch (const std::exception& e) {                                                            \
+        g_last_error = e.what();                                                                   \
+        return UAAMG_ECUDA;                                                                        \
+    }
+
+// host-only entry points: no CUDA runtime call (usable without a GPU)
+#define UA_HOST_TRY(...)               \
+    try {                              \
+        __VA_ARGS__;                   \
+        return UAAMG_OK;               \
+    } catch (const Error& e) {         \
+        g_last_error = e.what();       \
+        return e.code;                 \
+    }
+
+extern "C" {
+
+int uaamg_npcg_solve_sharded(uaamg_hierarchy* h, const uaamg_solve_params* p, int nranks, int64_t shard_rows,
+                             const double* b, const double* x0, double* x, double* history_host,
+                             uaamg_solve_result* res, void* stream) {
+    UA_TRY({
         std::memset(res, 0, sizeof(*res));
         std::lock_guard<std::mutex> lk(h->mu);
         StreamJoin join((cudaStream_t)stream, h->stream);
-        sharded_solve(h, *p, nranks, shard_rows, b, x0, x, history_host, res, h->stream);
-        const cudaError_t pe = cudaGetLastError();
-        if (pe != cudaSuccess) throw Error(UAAMG_ECUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
-        return UAAMG_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return UAAMG_ECUDA;
-    }
+        auto S = sharded_build(h, *p, nranks, -1, shard_rows, h->stream);
+        sharded_run(*S, b, x0, x, history_host, res);
+    })
 }
+
+int uaamg_dist_create(uaamg_hierarchy* h, const uaamg_solve_params* p, int rank, int nranks, int64_t shard_rows,
+                      uaamg_dist** out) {
+    UA_TRY({
+        if (rank < 0) throw Error(UAAMG_EINVAL, "rank must be >= 0");
+        auto d = std::make_unique<uaamg_dist>();
+        d->S = sharded_build(h, *p, nranks, rank, shard_rows, h->stream);
+        *out = d.release();
+    })
+}
+
+int uaamg_dist_handle(uaamg_dist* d, void* handle) {
+    UA_TRY({
+        cudaIpcMemHandle_t hd;
+        UA_CK(cudaIpcGetMemHandle(&hd, d->S->arena));
+        std::memcpy(handle, &hd, sizeof(hd));
+    })
+}
+
+int uaamg_dist_connect(uaamg_dist* d, const void* handles) {
+    UA_TRY({
+        Sharded& S = *d->S;
+        S.peer_base.assign(S.P, nullptr);
+        const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+        for (int q = 0; q < S.P; ++q) {
+            if (q == S.rank) {
+                S.peer_base[q] = S.arena;
+                continue;
+            }
+            void* ptr = nullptr;
+            UA_CK(cudaIpcOpenMemHandle(&ptr, hs[q], cudaIpcMemLazyEnablePeerAccess));
+            S.peer_base[q] = static_cast<char*>(ptr);
+        }
+        std::vector<double*> st(S.P);
+        std::vector<unsigned*> fl(S.P);
+        for (int q = 0; q < S.P; ++q) {
+            st[q] = reinterpret_cast<double*>(S.peer_base[q] + S.slots_off);
+            fl[q] = reinterpret_cast<unsigned*>(S.peer_base[q] + S.flags_off);
+        }
+        S.flag_tab.alloc(S.P, S.s);
+        UA_CK(cudaMemcpyAsync(S.slot_tab.p, st.data(), sizeof(double*) * S.P, cudaMemcpyHostToDevice, S.s));
+        UA_CK(cudaMemcpyAsync(S.flag_tab.p, fl.data(), sizeof(unsigned*) * S.P, cudaMemcpyHostToDevice, S.s));
+        UA_CK(cudaStreamSynchronize(S.s));
+    })
+}
+
+int uaamg_dist_solve(uaamg_dist* d, const double* b, const double* x0, double* x, double* history_host,
+                     uaamg_solve_result* res, void* stream) {
+    UA_TRY({
+        Sharded& S = *d->S;
+        if (S.peer_base.empty()) throw Error(UAAMG_EINVAL, "uaamg_dist_connect has not run");
+        std::memset(res, 0, sizeof(*res));
+        std::lock_guard<std::mutex> lk(S.h->mu);
+        StreamJoin join((cudaStream_t)stream, S.h->stream);
+        sharded_run(S, b, x0, x, history_host, res);
+    })
+}
+
+void uaamg_dist_free(uaamg_dist* d) { delete d; }
+
+int uaamg_partition_rows(int n, int nranks, int* bounds) {
+    UA_HOST_TRY({
+        if (nranks < 1 || nranks > kMaxRanks) throw Error(UAAMG_EINVAL, "ranks must be in [1, 8]");
+        const Part pt = level0_part(n, nranks);
+        for (int q = 0; q <= nranks; ++q) bounds[q] = pt.b[q];
+    })
+}
+
+int uaamg_partition_coarse(const int* seeds, int nc, const int* fine_bounds, int nranks, int* bounds) {
+    UA_HOST_TRY({
+        if (nranks < 1 || nranks > kMaxRanks) throw Error(UAAMG_EINVAL, "ranks must be in [1, 8]");
+        coarse_part(seeds, nc, fine_bounds, nranks, bounds);
+    })
+}
+
+}  // extern "C"
