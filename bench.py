@@ -10,8 +10,10 @@ Smoother(), b, tol=1e-8)``.  value = seconds per step (max over ranks).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 (torchrun, one rank per GPU): every rank solves its own copy of the
-problem (weak scaling, replicas -- the row-block partition is not built yet,
-see DESIGN.md); timing is the max over ranks of device time.
+problem (weak scaling, replicas); timing is the max over ranks of device
+time.  The row-partitioned multi-GPU solve (shard.cu)
+is validated by the tests; this harness has one GPU, so its scaling is not
+benchmarked here.
 ``--impl reference`` times the CPU oracle port of the reference path
 (oracle/, C + OpenMP, all host cores) on the same workload.
 """

@@ -17,12 +17,13 @@ for st in $STAGES; do
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
            python tools/one_solve.py > $OUT/ncu_launches.log 2>&1; echo "ncu rc=$?" >> $OUT/status.txt ;;
     ncufull)
-      # level-0 hot kernels of iteration 1: residual (first SrcPre1), fused
-      # up-sweep (31st SrcUp: 30 coarse-level cycles precede it), NPCG direction SpMV
-      for spec in "SrcPre1:0:resid" "SrcUp:30:upsweep" "EpiDirNpcg:0:dir"; do
+      # level-0 hot kernels of iteration 1 (TMA tile kernels): residual (first
+      # SrcVec/EpiResid TMA launch), post-sweep (2nd EpiSweepBeta TMA launch:
+      # the level-1 FCG step 2 precedes it), NPCG direction SpMV
+      for spec in "k_csr_tma<.*SrcVec.*EpiResid:0:resid" "k_csr_tma<.*SrcVec.*EpiSweepBeta:1:sweep" "k_csr_tma<.*EpiDirNpcg:0:dir"; do
         IFS=: read pat skip tag <<< "$spec"
         timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-          -k regex:$pat -s $skip -c 1 -o $OUT/prof_$tag python tools/one_solve.py > $OUT/ncu_full_$tag.log 2>&1
+          -k "regex:$pat" -s $skip -c 1 -o $OUT/prof_$tag python tools/one_solve.py > $OUT/ncu_full_$tag.log 2>&1
         echo "ncufull $tag rc=$?" >> $OUT/status.txt
       done ;;
   esac
