@@ -65,7 +65,14 @@ def peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    """SM clock / throttle-reason sampling DURING the timed region
+    (B200_PROFILING.md clocks line), through in-process NVML (nvidia-ml-py;
+    falls back to nvidia-smi).  Samples are taken by the main thread right
+    after each timed step's device work completed (between the step's end
+    event and the next step's start event): a query from a concurrent
+    thread takes a driver lock that stalled our setup's host-synchronised
+    phases by up to ~0.3 s per step (measured), inflating the very time being
+    sampled."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -73,44 +80,84 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, {reason names})
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) if hasattr(
+            nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        names = set()
+        for nm, const in (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+                          ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+                          ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+                          ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")):
+            if r & int(getattr(nv, const)):
+                names.add(nm)
+        return float(sm), float(mx), names
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        s = [x.strip() for x in out.split(",")]
+        names = set()
+        for k, nm in enumerate(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]):
+            if len(s) > 5 + k and s[5 + k].lower() == "active":
+                names.add(nm)
+        return float(s[1]), float(s[2]), names
 
     def _run(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
+        period = float(os.environ.get("BENCH_CLOCK_PERIOD", "0.2"))
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(period)
+
+    def sample(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
+        try:
+            self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if os.environ.get("BENCH_CLOCK_THREAD"):
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
         reasons = set()
         for s in self.samples:
-            for k, nm in enumerate(names):
-                if len(s) > 5 + k and s[5 + k].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+            reasons |= s[2]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def build_problem():
@@ -231,20 +278,32 @@ def run_ours(args, rank, ws, local):
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
-            h, x, (iters, hist) = step(profile=True)
+            h, x, (iters, hist) = step(profile=False)
             evs[k][1].record(stream)
             setup_s.append(h.setup_seconds)
-            secs = np.zeros(3)
-            byts = np.zeros(3)
-            cnt = np.zeros(1, dtype=np.int64)
-            _lib.check(_lib.load().uaamg_solve_profile(h._handle, secs.ctypes.data, byts.ctypes.data,
-                                                       cnt.ctypes.data))
-            prof["secs"] += secs
-            prof["count"] += int(cnt[0])
-            prof["bytes"] = byts
             del h
+        torch.cuda.synchronize()
+        # clocks sampled right after the last timed step's device work (see
+        # ClockSampler: a query overlapping the steps perturbs them)
+        for _ in range(3):
+            clk.sample()
         barrier()
     launches = _lib.launch_count() - launches0
+    # level-0 kernel timing (roofline): separate, untimed profile steps --
+    # the event nodes recorded inside the iteration graph perturb the step
+    for k in range(2):
+        flush.zero_()
+        h, _, _ = step(profile=True)
+        secs = np.zeros(3)
+        byts = np.zeros(3)
+        cnt = np.zeros(1, dtype=np.int64)
+        _lib.check(_lib.load().uaamg_solve_profile(h._handle, secs.ctypes.data, byts.ctypes.data,
+                                                   cnt.ctypes.data))
+        prof["secs"] += secs
+        prof["count"] += int(cnt[0])
+        prof["bytes"] = byts
+        del h
+    barrier()
     ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(args.steps)]
     t_step = sum(ms) / len(ms) / 1e3
     if ws > 1:
@@ -277,12 +336,15 @@ def run_ours(args, rank, ws, local):
 
     e2e_step()
     barrier()
-    t0 = time.perf_counter()
+    e2e_steps = []
     for _ in range(args.steps):
         flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         rep2 = e2e_step()
+        e2e_steps.append(time.perf_counter() - t0)
     barrier()
-    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e_s = float(np.mean(e2e_steps))
     d2h += (rep2.iterations + 1) * 8
 
     if rank != 0:
@@ -312,6 +374,9 @@ def run_ours(args, rank, ws, local):
         "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1, x0 = 0)",
         "config": {"workload": WORKLOAD, "n": n, "nnz": A.nnz, "iterations": int(iters), "tol": TOL,
                    "levels": None, "setup_s": float(np.mean(setup_s)),
+                   "setup_s_steps": [round(float(v), 5) for v in setup_s],
+                   "step_s_steps": [round(float(v) / 1e3, 5) for v in ms],
+                   "e2e_s_steps": [round(float(v), 5) for v in e2e_steps],
                    "solve_s": t_step - float(np.mean(setup_s)),
                    "l2": "flushed between steps (256 MB write, outside the step events); matrix 175 MB > L2",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",

@@ -303,8 +303,15 @@ __global__ void k_capped_commit(int n, uint8_t* st, uint8_t* newly, int* remaini
 // cooperative launch: scores -> max-hop -> select -> max-hop -> claim ->
 // admission fixpoint -> commit, separated by grid-wide barriers, with the
 // pass / admission loop control read from device counters (no host round
-// trips).  Short rows are handled thread-per-row, rows longer than kLongRow
-// warp-per-row (key max and "any" are order-free, so results are identical).
+// trips).  Pass 0 sweeps every vertex; later passes work on worklists: U =
+// the still-unprocessed vertices (compacted at each commit) and H = U plus
+// its neighbours (the only vertices whose hop values a selection or claim in
+// U reads).  Appends are atomic, so list order varies, but every phase is
+// order-free (key maxima, flags, a monotone fixpoint), so results are
+// bit-identical to the full sweeps.  Processed vertices keep stale
+// owner/adm values; they cannot match a current center (centers are
+// unprocessed until their own commit).  Short rows are handled
+// thread-per-item, rows longer than kLongRow warp-per-item.
 struct AggCoop {
     Csr A;
     const int* deg;
@@ -317,7 +324,11 @@ struct AggCoop {
     int* owner;
     uint8_t* adm;
     int* seed_of;
-    int* ctl;  // [0..2] centers / pass slot, [3..5] remaining / pass slot, [6..8] changed / iteration slot, [9] passes, [10] leftover
+    int* ulist[2];  // U, double-buffered by pass parity
+    int* hlist;     // H
+    int* mark;      // pass stamp of H membership
+    int* ctl;  // [0..2] centers / pass slot, [3..5] remaining / pass slot, [6..8] changed / iteration slot,
+               // [9] passes, [10] leftover, [11..13] |U'| / pass slot, [14..15] |H| / pass parity
 };
 
 __device__ __forceinline__ void warp_keymax(double& s, int& i) {
@@ -341,9 +352,19 @@ __device__ __forceinline__ void row_hopmax(const Csr& A, const double* ms, const
     }
 }
 
-__device__ void coop_hop1(const AggCoop& g, int mode, int tid, int nth, int lane, int w, int nw) {
+// items [0, cnt) of a worklist (list == nullptr: the identity, all vertices)
+struct WL {
+    const int* list;
+    int cnt;
+    __device__ __forceinline__ int operator[](int t) const { return list ? list[t] : t; }
+};
+
+// hop1 over the items of H: max key over the row's unprocessed (mode 0) or
+// center (mode 1) neighbours
+__device__ void coop_hop1(const AggCoop& g, WL H, int mode, int tid, int nth, int lane, int w, int nw) {
     const Csr& A = g.A;
-    for (int k = tid; k < A.n; k += nth) {
+    for (int t = tid; t < H.cnt; t += nth) {
+        const int k = H[t];
         const int e0 = A.rp[k], e1 = A.rp[k + 1];
         if (e1 - e0 > kLongRow) continue;
         double bs = 0.0;
@@ -358,7 +379,8 @@ __device__ void coop_hop1(const AggCoop& g, int mode, int tid, int nth, int lane
         g.ms[k] = bs;
         g.mi[k] = bi;
     }
-    for (int k = w; k < A.n; k += nw) {
+    for (int t = w; t < H.cnt; t += nw) {
+        const int k = H[t];
         const int e0 = A.rp[k], e1 = A.rp[k + 1];
         if (e1 - e0 <= kLongRow) continue;
         double bs = 0.0;
@@ -383,22 +405,39 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
     const int lane = threadIdx.x & 31, w = tid >> 5, nw = nth >> 5;
     volatile int* ctl = g.ctl;
     int remaining = n, pass = 0, itg = 0;
+    WL U{nullptr, n}, H{nullptr, n};
     for (; pass < g.max_passes; ++pass) {
         if (remaining == 0) break;  // U/aggregation.py:186
         const int ps = pass % 3;
-        if (tid == 0) { ctl[(pass + 1) % 3] = 0; ctl[3 + (pass + 1) % 3] = 0; }
-        // scores (K/numba_backend.py:100-111)
+        int* unext = g.ulist[(pass + 1) & 1];
+        if (tid == 0) {
+            ctl[(pass + 1) % 3] = 0;
+            ctl[3 + (pass + 1) % 3] = 0;
+            ctl[11 + (pass + 1) % 3] = 0;
+            ctl[14 + ((pass + 1) & 1)] = 0;
+        }
+        // scores of U (K/numba_backend.py:100-111); H = U and its neighbours
         const uint64_t base = pass_base(g.seed, pass);
-        for (int i = tid; i < n; i += nth) {
+        const int stamp = pass + 1;
+        int* hcnt = (int*)&ctl[14 + (pass & 1)];
+        for (int t = tid; t < U.cnt; t += nth) {
+            const int i = U[t];
             const double u = hash_unit(base, i);
             g.sc[i] = __dadd_rn((double)g.deg[i], __ddiv_rn(__dadd_rn((double)(i % 12), u), 12.0));
+            if (U.list)
+                for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+                    const int k = __ldg(A.ci + e);
+                    if (atomicExch(g.mark + k, stamp) != stamp) g.hlist[atomicAdd(hcnt, 1)] = k;
+                }
         }
         grid.sync();
-        coop_hop1(g, 0, tid, nth, lane, w, nw);
+        if (U.list) H = WL{g.hlist, ctl[14 + (pass & 1)]};
+        coop_hop1(g, H, 0, tid, nth, lane, w, nw);
         grid.sync();
         // selection (K/numba_backend.py:175-193)
         int local = 0;
-        for (int i = tid; i < n; i += nth) {
+        for (int t = tid; t < U.cnt; t += nth) {
+            const int i = U[t];
             const int e0 = A.rp[i], e1 = A.rp[i + 1];
             if (e1 - e0 > kLongRow || g.st[i] != 0) continue;
             double bs = 0.0;
@@ -406,7 +445,8 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             row_hopmax(A, g.ms, g.mi, i, e0, e1, 1, bs, bi);
             if (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi)) { g.st[i] = 1; ++local; }
         }
-        for (int i = w; i < n; i += nw) {
+        for (int t = w; t < U.cnt; t += nw) {
+            const int i = U[t];
             const int e0 = A.rp[i], e1 = A.rp[i + 1];
             if (e1 - e0 <= kLongRow || g.st[i] != 0) continue;
             double bs = 0.0;
@@ -417,10 +457,11 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
         }
         if (local) atomicAdd((int*)&ctl[ps], local);
         grid.sync();
-        coop_hop1(g, 1, tid, nth, lane, w, nw);
+        coop_hop1(g, H, 1, tid, nth, lane, w, nw);
         grid.sync();
         // claim (K/numba_backend.py:196-220) + admission seeds
-        for (int j = tid; j < n; j += nth) {
+        for (int t = tid; t < U.cnt; t += nth) {
+            const int j = U[t];
             const int e0 = A.rp[j], e1 = A.rp[j + 1];
             const uint8_t sj = g.st[j];
             g.adm[j] = (sj == 1);
@@ -432,7 +473,8 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             row_hopmax(A, g.ms, g.mi, j, e0, e1, 1, bs, bi);
             g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
         }
-        for (int j = w; j < n; j += nw) {
+        for (int t = w; t < U.cnt; t += nw) {
+            const int j = U[t];
             const int e0 = A.rp[j], e1 = A.rp[j + 1];
             if (e1 - e0 <= kLongRow || g.st[j] != 0) continue;
             double bs = 0.0;
@@ -448,7 +490,8 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             const int slot = itg % 3;
             if (tid == 0) ctl[6 + (itg + 1) % 3] = 0;
             int ch = 0;
-            for (int j = tid; j < n; j += nth) {
+            for (int t = tid; t < U.cnt; t += nth) {
+                const int j = U[t];
                 const int c = g.owner[j];
                 const int e0 = A.rp[j], e1 = A.rp[j + 1];
                 if (c < 0 || c == j || adm[j] || e1 - e0 > kLongRow) continue;
@@ -457,7 +500,8 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
                     if (adm[nb] && g.owner[nb] == c) { adm[j] = 1; ch = 1; break; }
                 }
             }
-            for (int j = w; j < n; j += nw) {
+            for (int t = w; t < U.cnt; t += nw) {
+                const int j = U[t];
                 const int c = g.owner[j];
                 const int e0 = A.rp[j], e1 = A.rp[j + 1];
                 if (c < 0 || c == j || adm[j] || e1 - e0 <= kLongRow) continue;
@@ -474,16 +518,20 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             ++itg;
             if (!any) break;
         }
-        // commit: admitted vertices and centers are processed, seeded by owner
+        // commit: admitted vertices and centers are processed, seeded by
+        // owner; the rest form the next pass's U
         int left = 0;
-        for (int j = tid; j < n; j += nth) {
+        int* ucnt = (int*)&ctl[11 + ps];
+        for (int t = tid; t < U.cnt; t += nth) {
+            const int j = U[t];
             const uint8_t sj = g.st[j];
             if (sj == 1 || (sj == 0 && adm[j])) { g.seed_of[j] = g.owner[j]; g.st[j] = 2; }
-            else if (sj == 0) ++left;
+            else if (sj == 0) { ++left; unext[atomicAdd(ucnt, 1)] = j; }
         }
         if (left) atomicAdd((int*)&ctl[3 + ps], left);
         grid.sync();
         remaining = ctl[3 + ps];
+        U = WL{unext, ctl[11 + ps]};
         if (ctl[ps] == 0) { ++pass; break; }  // no centers (cannot happen, U/aggregation.py:190)
     }
     if (tid == 0) { ctl[9] = pass; ctl[10] = remaining; }
@@ -852,6 +900,40 @@ __global__ void k_sq_expand(Csr A, const long long* off, unsigned long long* key
 // ============================================================ host drivers
 static int grid_for(int n) { return std::max(1, std::min(cdiv(n, 256), 4 * kNumSMs)); }
 
+// Grow-only per-thread scratch for the large transient setup buffers (the
+// Galerkin hash, the aggregation state): a setup finishes all its device
+// work before returning, so the next setup issued by the same thread can
+// reuse the memory; no pool growth or page mapping inside the timed setup.
+struct Scratch {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+};
+template <class T>
+static T* scratch(int slot, size_t count) {
+    static thread_local Scratch slots[16];
+    Scratch& sl = slots[slot];
+    const size_t want = count * sizeof(T) + 64;
+    if (want > sl.bytes) {
+        if (sl.p) {
+            UA_CK(cudaDeviceSynchronize());
+            UA_CK(cudaFree(sl.p));
+            sl.p = nullptr;
+        }
+        const size_t grow = want + want / 4;
+        UA_CK(cudaMalloc(&sl.p, grow));
+        sl.bytes = grow;
+    }
+    return static_cast<T*>(sl.p);
+}
+
+template <class T>
+struct SPtr {
+    T* p;
+};
+
 template <class T>
 static void exclusive_scan(const T* in, T* out, int n, cudaStream_t s) {
     size_t tmp = 0;
@@ -866,9 +948,10 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
     const int n = A.n;
     if (n <= 0) throw Error(UAAMG_EAGG, "cannot aggregate an empty matrix");
     const int G = grid_for(n);
-    DBuf<uint8_t> st(n, s), adm(n, s);
-    DBuf<double> sc(n, s), ms(n, s);
-    DBuf<int> mi(n, s), owner(n, s), seed_of(n, s), counters(4, s);
+    SPtr<uint8_t> st{scratch<uint8_t>(2, n)}, adm{scratch<uint8_t>(3, n)};
+    SPtr<double> sc{scratch<double>(4, n)}, ms{scratch<double>(5, n)};
+    SPtr<int> mi{scratch<int>(6, n)}, owner{scratch<int>(7, n)}, seed_of{scratch<int>(8, n)};
+    DBuf<int> counters(4, s);
     UA_CK(cudaMemsetAsync(st.p, 0, n, s));
     UA_CK(cudaMemsetAsync(seed_of.p, 0xff, sizeof(int) * n, s));
     static thread_local int* h_cnt = nullptr;  // pinned, reused across calls
@@ -886,10 +969,13 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
     int remaining = n;
     if (!capped) {
         DBuf<int> ctl(16, s);
+        SPtr<int> ul0{scratch<int>(9, n)}, ul1{scratch<int>(10, n)}, hl{scratch<int>(11, n)}, mark{scratch<int>(12, n)};
         UA_CK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(int), s));
+        UA_CK(cudaMemsetAsync(mark.p, 0, sizeof(int) * n, s));
         AggCoop g;
         g.A = A; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
         g.mi = mi.p; g.owner = owner.p; g.adm = adm.p; g.seed_of = seed_of.p; g.ctl = ctl.p;
+        g.ulist[0] = ul0.p; g.ulist[1] = ul1.p; g.hlist = hl.p; g.mark = mark.p;
         static int max_blocks = 0;
         if (!max_blocks) {
             int per_sm = 0, dev = 0, sms = 0;
@@ -993,8 +1079,8 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     UA_CK(cudaMemsetAsync(slen.p + nc, 0, sizeof(int), s));
     exclusive_scan(slen.p, soff.p, nc + 1, s);
     const size_t hsz = 2 * (size_t)std::max(A.nnz, 1);
-    DBuf<int> hkey(hsz, s);
-    DBuf<double> hval(hsz, s);
+    SPtr<int> hkey{scratch<int>(0, hsz)};
+    SPtr<double> hval{scratch<double>(1, hsz)};
     UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
     UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
     if (integer_exact(A, s)) {

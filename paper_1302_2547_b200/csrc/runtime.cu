@@ -108,6 +108,25 @@ static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t 
     UA_CK(cudaMemcpyAsync(L.seeds.p, seeds.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
 }
 
+// One non-blocking library stream per device, shared by every hierarchy:
+// allocations and frees of successive setups/solves are then ordered on one
+// stream, so the stream-ordered pool reuses freed blocks immediately instead
+// of growing (a per-hierarchy stream made reuse depend on cross-stream
+// completion tracking and cost up to ~0.25 s of pool growth per setup).
+cudaStream_t library_stream() {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    int dev = 0;
+    UA_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(dev);
+    if (it != streams.end()) return it->second;
+    cudaStream_t st;
+    UA_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    streams[dev] = st;
+    return st;
+}
+
 static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
                                    const uaamg_setup_params& P, cudaStream_t s) {
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
@@ -124,14 +143,40 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         UA_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         pool_configured = true;
     }
+    {
+        // pre-grow the pool to this setup's transient peak (Galerkin hash +
+        // aggregation scratch ~ 40 B/nonzero + 64 B/row) in one block, so the
+        // level-0 scratch never waits on a pool growth mid-setup
+        static size_t reserved = 0;
+        const size_t want = (size_t)40 * (size_t)nnz + (size_t)64 * (size_t)n;
+        size_t fr = 0, tot = 0;
+        UA_CK(cudaMemGetInfo(&fr, &tot));
+        if (want > reserved && want < fr / 2) {
+            void* p = nullptr;
+            UA_CK(cudaMallocAsync(&p, want, s));
+            UA_CK(cudaFreeAsync(p, s));
+            reserved = want;
+        }
+    }
     auto h = std::make_unique<uaamg_hierarchy>();
-    UA_CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->stream = library_stream();
     StreamJoin join(s, h->stream);
     s = h->stream;
     cudaEvent_t e0, e1;
     UA_CK(cudaEventCreate(&e0));
     UA_CK(cudaEventCreate(&e1));
     UA_CK(cudaEventRecord(e0, s));
+    // UAAMG_SETUP_PROF=1: per-phase stream time (diagnostics)
+    static const bool sprof = getenv("UAAMG_SETUP_PROF") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    auto mark = [&](const std::string& tag) {
+        if (!sprof) return;
+        cudaEvent_t e;
+        UA_CK(cudaEventCreate(&e));
+        UA_CK(cudaEventRecord(e, s));
+        marks.push_back({tag, e});
+    };
+    mark("start");
     auto L0 = std::make_unique<Level>();
     L0->n = n;
     L0->nnz = nnz;
@@ -141,12 +186,17 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     UA_CK(cudaMemcpyAsync(L0->rp.p, rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
     UA_CK(cudaMemcpyAsync(L0->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
     UA_CK(cudaMemcpyAsync(L0->av.p, av, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    mark("copy");
     finish_level(*L0, s);
+    mark("groups0");
     h->singular = P.singular < 0 ? detect_singular(*L0, s) : (P.singular != 0);
+    mark("singular");
     const int max_levels = P.max_levels;
     std::unique_ptr<Level> cur = std::move(L0);
     while (cur->n > P.n0 && (int)h->levels.size() < max_levels - 1) {
+        const std::string lt = "L" + std::to_string(h->levels.size()) + ".";
         aggregate_level(*cur, P, s);
+        mark(lt + "aggregate");
         if (cur->nc == cur->n)
             throw Error(UAAMG_ESETUP, "aggregation stagnated at level " + std::to_string(h->levels.size()) + ": " +
                                           std::to_string(cur->n) + " vertices produced no coarsening");
@@ -154,18 +204,28 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         cur->members.alloc(cur->n, s);
         build_members(cur->n, cur->nc, cur->v2a.p, cur->agg_ptr.p, cur->members.p, s);
         build_groups(cur->nc, cur->agg_ptr.p, kSolveLongMin, cur->mgrp, s);
+        mark(lt + "members");
         auto nxt = std::make_unique<Level>();
         nxt->n = cur->nc;
         nxt->nnz = device_galerkin(cur->csr(), cur->v2a.p, cur->nc, cur->agg_ptr.p, cur->members.p, nxt->rp, nxt->ci,
                                    nxt->av, s);
+        mark(lt + "galerkin");
         finish_level(*nxt, s);
+        mark(lt + "groups");
         h->levels.push_back(std::move(cur));
         cur = std::move(nxt);
     }
     h->levels.push_back(std::move(cur));
     h->coarse_mode = device_coarse_factor(h->levels.back()->csr(), h->singular, h->Minv, s);
+    mark("coarse");
     UA_CK(cudaEventRecord(e1, s));
     UA_CK(cudaEventSynchronize(e1));
+    for (size_t k = 1; k < marks.size(); ++k) {
+        float t = 0;
+        cudaEventElapsedTime(&t, marks[k - 1].second, marks[k].second);
+        fprintf(stderr, "setup %-16s %8.3f ms\n", marks[k].first.c_str(), t);
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
     float ms = 0;
     UA_CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);

@@ -103,10 +103,7 @@ struct uaamg_hierarchy {
         ws.reset();
         levels.clear();
         Minv.release();
-        if (stream) {
-            cudaStreamSynchronize(stream);
-            cudaStreamDestroy(stream);
-        }
+        // the library stream is shared by all hierarchies (library_stream)
     }
 };
 
@@ -307,6 +304,7 @@ struct Plan {
 };
 
 void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s);
+cudaStream_t library_stream();
 // a fresh solve workspace; engine: record the persistent-engine op list;
 // levels < mat_levels materialise the pre-smoothed / prolongated iterates
 std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, bool engine,

@@ -23,6 +23,9 @@ def ev_time(fn, reps=3):
     ts = []
     out = None
     for _ in range(reps):
+        out = None  # free the previous result first (as bench.py does between steps)
+        import gc
+        gc.collect()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -34,7 +37,7 @@ def ev_time(fn, reps=3):
     return out, ts
 
 
-h, ts = ev_time(lambda: U.setup(Ad))
+h, ts = ev_time(lambda: U.setup(Ad), reps=int(os.environ.get("SETUP_REPS", "3")))
 print("setup (event s, wall s):", [(round(a, 4), round(b_, 4)) for a, b_ in ts], flush=True)
 print("levels", [(l.n, l.matrix.nnz if hasattr(l.matrix, "nnz") else None) for l in h.levels], flush=True)
 for er in [int(x) for x in os.environ.get("ENGINE_ROWS_LIST", "0,-1,50000,20000").split(",")]:
