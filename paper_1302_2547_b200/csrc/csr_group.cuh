@@ -122,6 +122,22 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
 template <class Src, class Epi, bool Unit>
 __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, Src src_p, Epi epi_p) {
     __shared__ double win[kGrpWarps][kGrpRound];
+    {
+        // before the dependency wait: pull this warp's first row group of the
+        // (read-only) matrix into L1 while the predecessor kernel drains
+        const int u0 = blockIdx.x * kGrpWarps + (threadIdx.x >> 5);
+        if (u0 < G.ng) {
+            const int lane = threadIdx.x & 31;
+            const int r0 = G.base + (u0 << 5);
+            const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + G.base + min((u0 << 5) + 32, G.n));
+            const int cb = (e0 * 4) & ~127, ce = e1 * 4;  // col bytes [cb, ce)
+            for (int o = cb + lane * 128; o < ce; o += 32 * 128) pf(reinterpret_cast<const char*>(A.ci) + o);
+            if (!Unit) {
+                const long long vb = ((long long)e0 * 8) & ~127ll, ve = (long long)e1 * 8;
+                for (long long o = vb + lane * 128; o < ve; o += 32 * 128) pf(reinterpret_cast<const char*>(A.av) + o);
+            }
+        }
+    }
     pdl_wait();
     pdl_trigger();
     Epi epi = epi_p;

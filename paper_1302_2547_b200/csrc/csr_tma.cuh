@@ -63,15 +63,8 @@ __device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15
 template <class Src, class Epi, bool Unit>
 __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, int ntiles, int cap, Src src_p, Epi epi_p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    pdl_wait();
-    pdl_trigger();
     Epi epi = epi_p;
-    if (!epi.gate()) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) epi.off();
-        return;
-    }
     Src src = src_p;
-    src.init();
     const TmaLayout Ly = tma_layout(cap);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kTmaStages * Ly.stage);
     const int t = threadIdx.x;
@@ -106,10 +99,8 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
         e1 = __ldg(A.rp + min(r0 + kTmaRows, end));
     };
     int ne0 = 0, ne1 = 0;  // producer: bounds of the next tile to issue
-    if (my > 0 && base + blockIdx.x * kTmaRows + t < end) {
-        epi.pre(base + blockIdx.x * kTmaRows + t);
-        src.pre(base + blockIdx.x * kTmaRows + t);
-    }
+    // the matrix is read-only: its first tiles stream in before the
+    // dependency wait, overlapping the predecessor kernel's tail (PDL)
     if (t == 0) {
         for (int j = 0; j < min(my, kTmaStages - 1); ++j) {
             int e0, e1;
@@ -117,6 +108,20 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
             issue(j, e0, e1);
         }
         if (kTmaStages - 1 < my) bounds(kTmaStages - 1, ne0, ne1);
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (!epi.gate()) {
+        // gated off: drain the bulk copies already issued before leaving
+        for (int j = 0; j < min(my, kTmaStages - 1); ++j) mbar_wait(&mbar[j % kTmaStages], 0);
+        if (blockIdx.x == 0 && threadIdx.x == 0) epi.off();
+        return;
+    }
+    src.init();
+    // per-row operands may have been written by the predecessor: after the wait
+    if (my > 0 && base + blockIdx.x * kTmaRows + t < end) {
+        epi.pre(base + blockIdx.x * kTmaRows + t);
+        src.pre(base + blockIdx.x * kTmaRows + t);
     }
     // Software pipeline over this CTA's tiles: iteration j folds tile j
     // (products already in its stage) while the gathers of tile j + 1 are

@@ -329,6 +329,7 @@ struct AggCoop {
     int* mark;      // pass stamp of H membership
     int* ctl;  // [0..2] centers / pass slot, [3..5] remaining / pass slot, [6..8] changed / iteration slot,
                // [9] passes, [10] leftover, [11..13] |U'| / pass slot, [14..15] |H| / pass parity
+    unsigned long long* prof;  // diagnostics (UAAMG_AGG_PROF): per pass {t_start, |U|, |H|, admission iterations}
 };
 
 __device__ __forceinline__ void warp_keymax(double& s, int& i) {
@@ -416,6 +417,13 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             ctl[11 + (pass + 1) % 3] = 0;
             ctl[14 + ((pass + 1) & 1)] = 0;
         }
+        if (g.prof && tid == 0 && pass < 32) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            g.prof[4 * pass] = t;
+            g.prof[4 * pass + 1] = U.cnt;
+        }
+        const int itg0 = itg;
         // scores of U (K/numba_backend.py:100-111); H = U and its neighbours
         const uint64_t base = pass_base(g.seed, pass);
         const int stamp = pass + 1;
@@ -530,11 +538,20 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
         }
         if (left) atomicAdd((int*)&ctl[3 + ps], left);
         grid.sync();
+        if (g.prof && tid == 0 && pass < 32) {
+            g.prof[4 * pass + 2] = H.cnt;
+            g.prof[4 * pass + 3] = itg - itg0;
+        }
         remaining = ctl[3 + ps];
         U = WL{unext, ctl[11 + ps]};
         if (ctl[ps] == 0) { ++pass; break; }  // no centers (cannot happen, U/aggregation.py:190)
     }
     if (tid == 0) { ctl[9] = pass; ctl[10] = remaining; }
+    if (g.prof && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g.prof[4 * min(pass, 32)] = t;
+    }
 }
 
 // ============================================================ renumbering
@@ -976,6 +993,14 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         g.A = A; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
         g.mi = mi.p; g.owner = owner.p; g.adm = adm.p; g.seed_of = seed_of.p; g.ctl = ctl.p;
         g.ulist[0] = ul0.p; g.ulist[1] = ul1.p; g.hlist = hl.p; g.mark = mark.p;
+        static const bool aprof = getenv("UAAMG_AGG_PROF") != nullptr;
+        DBuf<unsigned long long> prof;
+        g.prof = nullptr;
+        if (aprof) {
+            prof.alloc(4 * 33, s);
+            UA_CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * 4 * 33, s));
+            g.prof = prof.p;
+        }
         static int max_blocks = 0;
         if (!max_blocks) {
             int per_sm = 0, dev = 0, sms = 0;
@@ -984,6 +1009,8 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
             UA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             max_blocks = std::max(1, per_sm) * sms;
         }
+        // one vertex per thread up to full residency: the passes are
+        // latency-bound, fewer CTAs (cheaper barriers) measured slower
         const int blocks = std::max(1, std::min(max_blocks, cdiv(n, 256)));
         void* args[] = {&g};
         UA_CK(cudaLaunchCooperativeKernel((void*)k_aggregate_coop, blocks, 256, args, 0, s));
@@ -993,6 +1020,14 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         passes = h_cnt[0];
         remaining = h_cnt[1];
         max_passes = 0;  // skip the host-driven loop below
+        if (aprof) {
+            unsigned long long hp[4 * 33];
+            UA_CK(cudaMemcpy(hp, prof.p, sizeof(hp), cudaMemcpyDeviceToHost));
+            fprintf(stderr, "aggregate n=%d blocks=%d passes=%d\n", n, blocks, passes);
+            for (int k = 0; k < std::min(passes, 32); ++k)
+                fprintf(stderr, "  pass %2d |U| %9llu |H| %9llu adm-it %2llu  %8.1f us\n", k, hp[4 * k + 1],
+                        hp[4 * k + 2], hp[4 * k + 3], (hp[4 * (k + 1)] - hp[4 * k]) * 1e-3);
+        }
     }
     for (int pass = 0; pass < max_passes; ++pass) {
         if (remaining == 0) break;  // U/aggregation.py:186
