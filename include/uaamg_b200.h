@@ -223,6 +223,15 @@ int uaamg_dist_solve(uaamg_dist *d, const double *b, const double *x0, double *x
                      uaamg_solve_result *res, void *stream);
 void uaamg_dist_free(uaamg_dist *d);
 
+/* On-device generator of the 3D lattice Laplacians of the benchmark configs
+ * (C2/C4/C5), bit-identical to the host builder
+ * problems.grid3d / the reference's assemble_laplacian: box nx*ny*nz,
+ * vertex (x*ny + y)*nz + z, stencil 7 or 27, unit weights, Dirichlet by
+ * elimination (neumann = 0) or Neumann.  Two passes: col == NULL writes
+ * row_ptr (n+1) and returns *nnz; then col/val (nnz each) are filled. */
+int uaamg_gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int *row_ptr, int *col, double *val,
+                     int64_t *nnz, void *stream);
+
 /* Row partitions used by the sharded solve (host-only helpers):
  * level 0 in equal 128-row-aligned contiguous blocks; a coarse level by seed
  * ownership (aggregates are numbered by ascending seed, so rank q owns the

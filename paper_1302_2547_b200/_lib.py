@@ -88,6 +88,7 @@ _SIGS = {
     "uaamg_dist_solve": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
     "uaamg_dist_free": (None, [_vp]),
     "uaamg_partition_rows": (_i, [_i, _i, _vp]),
+    "uaamg_gen_grid3d": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "uaamg_partition_coarse": (_i, [_vp, _i, _vp, _i, _vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),

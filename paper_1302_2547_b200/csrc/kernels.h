@@ -158,6 +158,10 @@ void launch_npcg_init(int n, const double* b, const double* r, NpcgState* st, do
 void launch_copy(int n, const double* src, double* dst, cudaStream_t s);
 void launch_axpby_init(int n, const double* b, const double* ax, double* r, cudaStream_t s);  // r = b - ax
 
+// on-device 3D lattice Laplacian: pass 1 (ci == nullptr) writes row_ptr and
+// returns nnz; pass 2 fills col / val
+long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av, cudaStream_t s);
+
 // ---- setup kernels (kernels_setup.cu) ----
 void launch_degrees(const Csr& A, int* deg, cudaStream_t s);
 void launch_scores(const Csr& A, const int* deg, uint64_t seed, int64_t pass_idx, double* scores, cudaStream_t s);

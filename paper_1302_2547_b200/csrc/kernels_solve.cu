@@ -383,3 +383,74 @@ void launch_axpby_init(int n, const double* b, const double* ax, double* r, cuda
 }
 
 }  // namespace uaamg
+
+// ============================================================ problem generation
+// On-device 3D lattice Laplacian: the canonical CSR
+// that paper_1302_2547_b200/problems.py:grid3d builds on the host (itself
+// bit-identical to the reference's assemble_laplacian(GraphProblem(...)),
+// U/graph.py:63-82, U/sparse.py:56-74): vertex i = (x*ny + y)*nz + z, columns
+// ascending (offsets dx outer, dz inner), off-diagonals -1, diagonal
+// stencil-1 (Dirichlet by elimination) or the degree (Neumann).
+namespace uaamg {
+namespace {
+__device__ __forceinline__ int grid_nbrs(int x, int y, int z, int nx, int ny, int nz, int stencil, int* off,
+                                         long long sxy, int sy) {
+    int k = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dz = -1; dz <= 1; ++dz) {
+                if (stencil == 7 && abs(dx) + abs(dy) + abs(dz) > 1) continue;
+                if ((dx < 0 && x == 0) || (dx > 0 && x == nx - 1) || (dy < 0 && y == 0) || (dy > 0 && y == ny - 1) ||
+                    (dz < 0 && z == 0) || (dz > 0 && z == nz - 1))
+                    continue;
+                if (off) off[k] = (int)(dx * sxy + dy * sy + dz);
+                ++k;
+            }
+    return k;
+}
+__global__ void k_grid_count(int nx, int ny, int nz, int stencil, int* cnt) {
+    const long long n = (long long)nx * ny * nz;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int z = (int)(i % nz), y = (int)((i / nz) % ny), x = (int)(i / ((long long)ny * nz));
+        cnt[i + 1] = grid_nbrs(x, y, z, nx, ny, nz, stencil, nullptr, (long long)ny * nz, nz);
+        if (i == 0) cnt[0] = 0;
+    }
+}
+__global__ void k_grid_fill(int nx, int ny, int nz, int stencil, int neumann, const int* rp, int* ci, double* av) {
+    const long long n = (long long)nx * ny * nz;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int z = (int)(i % nz), y = (int)((i / nz) % ny), x = (int)(i / ((long long)ny * nz));
+        int off[27];
+        const int k = grid_nbrs(x, y, z, nx, ny, nz, stencil, off, (long long)ny * nz, nz);
+        const double diag = neumann ? (double)(k - 1) : (double)(stencil - 1);
+        int p = rp[i];
+        for (int q = 0; q < k; ++q, ++p) {
+            ci[p] = (int)(i + off[q]);
+            av[p] = off[q] == 0 ? diag : -1.0;
+        }
+    }
+}
+}  // namespace
+
+long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av,
+                     cudaStream_t s) {
+    const long long n = (long long)nx * ny * nz;
+    if (n <= 0 || n > 0x7fffffffll) throw Error(UAAMG_EINVAL, "grid size out of range");
+    if (stencil != 7 && stencil != 27) throw Error(UAAMG_EINVAL, "stencil must be 7 or 27");
+    const int grid = std::min(cdiv(n, 256), 8 * kNumSMs);
+    if (!ci) {
+        // pass 1: row_ptr (counts + inclusive scan), returns nnz
+        UA_LAUNCH(k_grid_count, grid, 256, 0, s, nx, ny, nz, stencil, rp);
+        size_t tmp = 0;
+        UA_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, rp + 1, rp + 1, (int)n, s));
+        DBuf<char> t(tmp, s);
+        UA_CK(cub::DeviceScan::InclusiveSum(t.p, tmp, rp + 1, rp + 1, (int)n, s));
+        int nnz = 0;
+        UA_CK(cudaMemcpyAsync(&nnz, rp + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        return nnz;
+    }
+    UA_LAUNCH(k_grid_fill, grid, 256, 0, s, nx, ny, nz, stencil, neumann, rp, ci, av);
+    return -1;
+}
+}  // namespace uaamg

@@ -77,18 +77,21 @@ def grid2d(n, bc="dirichlet", anisotropy=(1.0, 1.0)):
     return SparseMatrix(N, N, ip, ix, a, _validate=False)
 
 
-def grid3d(n, stencil=7, bc="dirichlet"):
+def grid3d(n, stencil=7, bc="dirichlet", dims=None):
     """3D lattice Laplacian, unit weights; 7-point (face neighbours) or
     27-point (all 26 neighbours).  Dirichlet by elimination: every vertex
     gets boundary weight = number of missing stencil neighbours, so the
-    diagonal is 6 / 26 everywhere."""
+    diagonal is 6 / 26 everywhere.  ``dims``
+    (nx, ny, nz) builds a box instead of the n^3 cube (vertex
+    (x*ny + y)*nz + z)."""
     if stencil not in (7, 27):
         raise ValueError("stencil must be 7 or 27")
-    if n < 2:
+    nx, ny, nz = dims if dims is not None else (n, n, n)
+    if min(nx, ny, nz) < 2:
         raise ValueError("grid size must be >= 2")
-    N = n ** 3
+    N = nx * ny * nz
     v = np.arange(N, dtype=np.int64)
-    x, y, z = v // (n * n), (v // n) % n, v % n
+    x, y, z = v // (ny * nz), (v // nz) % ny, v % nz
     del v
     offs, valid = [], []
     for dx in (-1, 0, 1):
@@ -97,12 +100,12 @@ def grid3d(n, stencil=7, bc="dirichlet"):
                 if stencil == 7 and abs(dx) + abs(dy) + abs(dz) > 1:
                     continue
                 m = np.ones(N, dtype=bool)
-                for d, c in ((dx, x), (dy, y), (dz, z)):
+                for d, c, nd in ((dx, x, nx), (dy, y, ny), (dz, z, nz)):
                     if d < 0:
                         m &= c > 0
                     elif d > 0:
-                        m &= c < n - 1
-                offs.append(dx * n * n + dy * n + dz)
+                        m &= c < nd - 1
+                offs.append(dx * ny * nz + dy * nz + dz)
                 valid.append(m)
     deg = np.zeros(N)
     for o, m in zip(offs, valid):
@@ -114,6 +117,35 @@ def grid3d(n, stencil=7, bc="dirichlet"):
         diag = deg
     ip, ix, a = _csr_from_offsets(valid, offs, [1.0] * len(offs), diag)
     return SparseMatrix(N, N, ip, ix, a, _validate=False)
+
+
+def grid3d_device(n, stencil=7, bc="dirichlet", dims=None):
+    """``grid3d`` built directly on the device (csrc: gen_grid3d) as a
+    DeviceCSR -- same bits as the host builder, no host assembly (the host
+    path needs tens of GB and minutes at the 256^3 / 512^3 configs)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import DeviceCSR, cuda_device, ptr, stream
+
+    if stencil not in (7, 27):
+        raise ValueError("stencil must be 7 or 27")
+    if bc not in ("dirichlet", "neumann"):
+        raise ValueError(f"unknown boundary condition {bc!r}")
+    nx, ny, nz = dims if dims is not None else (n, n, n)
+    N = nx * ny * nz
+    dev = cuda_device()
+    rp = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    nnz = ctypes.c_int64()
+    L = _lib.load()
+    neu = int(bc == "neumann")
+    _lib.check(L.uaamg_gen_grid3d(nx, ny, nz, stencil, neu, ptr(rp), None, None, ctypes.byref(nnz), stream()))
+    ci = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+    av = torch.empty(nnz.value, dtype=torch.float64, device=dev)
+    _lib.check(L.uaamg_gen_grid3d(nx, ny, nz, stencil, neu, ptr(rp), ptr(ci), ptr(av), None, stream()))
+    return DeviceCSR(N, N, rp, ci, av)
 
 
 def random_geometric(N, degree=12.0, seed=0, return_edges=False):

@@ -235,3 +235,15 @@ def test_c2_full_size_hierarchy_and_history(U):
     assert_hierarchy_equal(g, _gpu_levels(h))
     x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=1e-8, max_iters=500)
     assert_history_close(rep.residual_history, g, rtol=RTOL)
+
+
+@pytest.mark.parametrize("dims,stencil,bc", [((5, 5, 5), 7, "dirichlet"), ((6, 4, 5), 27, "dirichlet"),
+                                             ((4, 7, 3), 7, "neumann"), ((5, 6, 4), 27, "neumann")])
+def test_device_grid_generator_matches_host(U, dims, stencil, bc):
+    """On-device 3D lattice builder == host builder (== reference assembly)."""
+    from paper_1302_2547_b200 import problems
+
+    h = problems.grid3d(None, stencil, bc, dims=dims)
+    d = problems.grid3d_device(None, stencil, bc, dims=dims).to_host()
+    assert np.array_equal(h.indptr, d.indptr) and np.array_equal(h.indices, d.indices)
+    assert np.array_equal(h.data, d.data)

@@ -1,0 +1,120 @@
+"""Single-GPU runs of the BASELINE.json configs beyond the bench line (C1, C3,
+C4; C2 is bench.py): device setup + NPCG solve to 1e-8 (b = 1, x0 = 0),
+CUDA-event times, iterations, hierarchy, level-0 kernel roofline fractions.
+Grids are generated on the device (problems.grid3d_device); the random
+geometric graph (C3) on the host.  Optionally the row-partitioned solve with
+P virtual ranks is checked against the single-device history.
+
+  python tools/configs_bench.py [C1 C3 C4 ...] [--sharded P]
+"""
+import ctypes
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1302_2547_b200 as U  # noqa: E402
+from paper_1302_2547_b200 import _lib, problems  # noqa: E402
+from paper_1302_2547_b200.device import DeviceCSR  # noqa: E402
+from paper_1302_2547_b200.solvers import _params  # noqa: E402
+
+PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                         "MEASURED_PEAKS.json")))["hbm_gbs"]) if os.path.exists(
+    os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6442.9
+
+
+def build(name):
+    t = time.perf_counter()
+    if name == "C1":
+        A = DeviceCSR.from_host(problems.grid2d(256))
+        desc = "2D 5-point 256^2"
+    elif name == "C2":
+        A = problems.grid3d_device(128, 7)
+        desc = "3D 7-point 128^3"
+    elif name == "C3":
+        A = DeviceCSR.from_host(problems.random_geometric(1 << 23, 12.0, seed=0))
+        desc = "random geometric graph, 8,388,608 vertices, degree ~12"
+    elif name == "C4":
+        A = problems.grid3d_device(256, 27)
+        desc = "3D 27-point 256^3 (single GPU)"
+    elif name == "C5x":
+        A = problems.grid3d_device(None, 7, dims=(512, 512, 64))
+        desc = "3D 7-point 512x512x64 (1/8 of C5: one GPU's slab)"
+    else:
+        raise ValueError(name)
+    torch.cuda.synchronize()
+    return A, desc, time.perf_counter() - t
+
+
+def solve(h, b, profile):
+    n = b.shape[0]
+    P = _params(U.CycleSpec(), U.Smoother(), 1e-8, 500, True)
+    P.profile_level0 = int(profile)
+    res = _lib.SolveResult()
+    x = torch.empty(n, dtype=torch.float64, device=b.device)
+    hist = np.zeros(501)
+    _lib.check(_lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), b.data_ptr(), None, x.data_ptr(),
+                                            hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
+                                            torch.cuda.current_stream().cuda_stream))
+    return x, res, hist[: res.iterations + 1]
+
+
+def run(name, sharded):
+    A, desc, tgen = build(name)
+    n = A.n_rows
+    b = torch.ones(n, dtype=torch.float64, device="cuda")
+    h = U.setup(A)
+    x, res, hist = solve(h, b, False)  # warm-up (graphs, pools)
+    del h
+    steps = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        h = U.setup(A)
+        x, res, hist = solve(h, b, False)
+        e1.record()
+        torch.cuda.synchronize()
+        steps.append((e0.elapsed_time(e1) * 1e-3, h.setup_seconds, res.solve_seconds))
+        if len(steps) < 3:
+            del h
+    _, rp, _ = solve(h, b, True)
+    secs, byts, cnt = np.zeros(3), np.zeros(3), np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.load().uaamg_solve_profile(h._handle, secs.ctypes.data, byts.ctypes.data, cnt.ctypes.data))
+    kern = {}
+    for i, nm in enumerate(["residual", "post_sweep", "direction_spmv"]):
+        if cnt[0] and secs[i] > 0:
+            per = secs[i] / cnt[0]
+            kern[nm] = {"us": round(per * 1e6, 1), "GBps": round(byts[i] / per / 1e9, 1),
+                        "frac": round(byts[i] / per / 1e9 / PEAK, 3)}
+    r = A.spmv(x) - b
+    relres = float(torch.linalg.norm(r) / torch.linalg.norm(b))
+    best = min(steps)
+    out = {"config": name, "workload": desc, "n": n, "nnz": A.nnz, "generate_s": round(tgen, 2),
+           "levels": [lv.n for lv in h.levels], "iterations": int(res.iterations), "true_relres": relres,
+           "step_s_best": round(best[0], 4), "setup_s": round(best[1], 4), "solve_s": round(best[2], 4),
+           "steps_s": [round(s[0], 4) for s in steps], "level0_kernels": kern,
+           "grid_complexity": round(h.grid_complexity, 4), "operator_complexity": round(h.operator_complexity, 4)}
+    if sharded:
+        xs, rs = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500, ranks=sharded)
+        h1 = np.asarray(hist)
+        hs = np.asarray(rs.residual_history)
+        out["sharded"] = {"ranks": sharded, "iterations": rs.iterations,
+                          "max_rel_history_diff": float(np.max(np.abs(hs - h1) / np.maximum(h1, 1e-300)))
+                          if hs.shape == h1.shape else None}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:]
+    sh = 0
+    if "--sharded" in args:
+        k = args.index("--sharded")
+        sh = int(args[k + 1])
+        del args[k:k + 2]
+    for c in args or ["C1", "C4"]:
+        run(c, sh)
