@@ -223,6 +223,39 @@ def cpu_baseline_sample(A):
                       "CPU oracle C/OpenMP"}
 
 
+def level0_c5_slab(U, _lib, dev):
+    """Level-0 kernel roofline at the north star's per-GPU size: one GPU's
+    slab of C5 (3D 7-point 512 x 512 x 64 = 16.8M rows), generated on the
+    device; one warm solve, then one profiled solve (CUDA events inside the
+    iteration graph).  Supplementary to the C2 line; not part of `value`."""
+    import ctypes
+    import torch
+    from paper_1302_2547_b200 import problems
+    from paper_1302_2547_b200.solvers import _params
+    A = problems.grid3d_device(None, 7, dims=(512, 512, 64))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device=dev)
+    h = U.setup(A)
+    peak, _ = peak_hbm()
+    out = {}
+    for profile in (0, 1):
+        P = _params(U.CycleSpec(), U.Smoother(), TOL, 500, True)
+        P.profile_level0 = profile
+        res = _lib.SolveResult()
+        x = torch.empty(A.n_rows, dtype=torch.float64, device=dev)
+        _lib.check(_lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), b.data_ptr(), None, x.data_ptr(), None,
+                                                ctypes.byref(res), torch.cuda.current_stream().cuda_stream))
+    secs, byts, cnt = np.zeros(3), np.zeros(3), np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.load().uaamg_solve_profile(h._handle, secs.ctypes.data, byts.ctypes.data, cnt.ctypes.data))
+    for i, nm in enumerate(["residual", "post_sweep", "direction_spmv"]):
+        if cnt[0] and secs[i] > 0:
+            per = secs[i] / cnt[0]
+            out[nm] = {"us_per_launch": per * 1e6, "GBps": byts[i] / per / 1e9, "frac": byts[i] / per / 1e9 / peak,
+                       "bytes_per_launch": float(byts[i])}
+    out["workload"] = "3D 7-point 512x512x64 (one GPU's slab of C5), %d iterations" % res.iterations
+    del h
+    return out
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, rank, ws, local):
     import torch
@@ -367,6 +400,7 @@ def run_ours(args, rank, ws, local):
         except Exception:
             traffic = None
     cpu = cpu_baseline_sample(A) if ws == 1 else None
+    slab = level0_c5_slab(U, _lib, dev) if ws == 1 else None
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3, "higher_is_better": False,
@@ -380,7 +414,8 @@ def run_ours(args, rank, ws, local):
                    "solve_s": t_step - float(np.mean(setup_s)),
                    "l2": "flushed between steps (256 MB write, outside the step events); matrix 175 MB > L2",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                   "true_relres": relres, "level0_kernels": kern},
+                   "true_relres": relres, "level0_kernels": kern,
+                   "level0_kernels_c5_slab": slab},
         "roofline": {"bound": "hbm", "kernel": "level-0 l1-Jacobi post-sweep (TMA tiles) with the fused NPCG beta dot",
                      "achieved": dom.get("GBps"), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": dom.get("frac"), "traffic": traffic},
