@@ -182,7 +182,8 @@ __device__ __noinline__ void run_dense(Ctx& c, const Op* op) {
 __global__ void __launch_bounds__(kEngThreads, 1) k_engine(EngineArgs a) {
     __shared__ double sm[kEngThreads / 32 + 1];
     __shared__ double tot[kEngK];
-    __shared__ __align__(16) Op chunk[kOpChunk];
+    __shared__ __align__(16) unsigned char chunk_raw[kOpChunk * sizeof(Op)];
+    Op* chunk = reinterpret_cast<Op*>(chunk_raw);
     __shared__ double win[(kEngThreads / 32) * kGrpRound];
     if (a.gate && *(volatile const int*)a.gate == 0) return;
     Ctx c{(int)gridDim.x, false, {0, 0}, sm, tot, a.partials, a.bar, win};

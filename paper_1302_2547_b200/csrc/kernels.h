@@ -109,6 +109,11 @@ void launch_restrict_exact(int nc, const int* agg_ptr, const int* members, const
 // r = b - A x, x given (xmode 2) or implicit one sweep from zero (xmode 1) or zero (xmode 0)
 void launch_residual(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
                      const double* x, double* r, const int* gate, Exec ex);
+// residual fused with the restriction into a single-aggregate coarsest level
+// and its 1x1 solve: rc = sum(r), ec = minv[0] * rc
+void launch_residual_sum(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
+                         const double* x, double* r, double* rc, double* ec, const double* minv, const int* gate,
+                         RedScratch rs, Exec ex);
 // one Jacobi/l1 sweep: out = x + invm (b - A x), x from a vector
 void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
                       double* out, const int* gate, Exec ex, const BetaReq* br = nullptr, RedScratch rs = {});

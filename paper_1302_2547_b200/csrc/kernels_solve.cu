@@ -54,6 +54,16 @@ static EpiSweepBeta sweep_beta(const double* invm, const double* b, double* out,
     return e;
 }
 
+void launch_residual_sum(const Csr& A, const Groups& G, int xmode, const double* invm, const double* b,
+                         const double* x, double* r, double* rc, double* ec, const double* minv, const int* gate,
+                         RedScratch rs, Exec ex) {
+    EpiResidSum e{};
+    e.b = b; e.r = r; e.g = gate; e.rc = rc; e.ec = ec; e.minv = minv; e.red = {rs.partials, rs.ticket};
+    if (xmode == 1) run_stream<SrcPre1, EpiResidSum, false>(A, G, SrcPre1{invm, b}, e, ex);
+    else if (xmode == 0) run_stream<SrcZero, EpiResidSum, false>(A, G, SrcZero{}, e, ex);
+    else run_stream<SrcVec, EpiResidSum, false>(A, G, SrcVec{x}, e, ex);
+}
+
 void launch_sweep_vec(const Csr& A, const Groups& G, const double* invm, const double* b, const double* x,
                       double* out, const int* gate, Exec ex, const BetaReq* br, RedScratch rs) {
     if (br) {

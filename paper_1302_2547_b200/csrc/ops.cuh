@@ -34,7 +34,10 @@ struct DenseArgs {
     X(7, SrcDir, EpiDirFcg, false)            \
     X(8, SrcUp, EpiSweepBeta, false)          \
     X(9, SrcVec, EpiSweepBeta, false)         \
-    X(10, SrcVec, EpiRestrictBegin, true)
+    X(10, SrcVec, EpiRestrictBegin, true)     \
+    X(11, SrcPre1, EpiResidSum, false)        \
+    X(12, SrcVec, EpiResidSum, false)         \
+    X(13, SrcZero, EpiResidSum, false)
 //   X(kind, Body)
 #define UA_ENGINE_MAP_OPS(X) \
     X(20, BodyXpre1)         \

@@ -186,6 +186,24 @@ struct Plan {
             }
             xpre = cur;
         }
+        LevelWs& C = ws->lev[l + 1];
+        const bool exact = (l + 1 == coarsest());
+        // coarsest level = one aggregate: residual, restriction (a sum) and
+        // the 1x1 solve in one kernel
+        if (exact && L.nc == 1 && !sing() && l > 0) {
+            launch_residual_sum(A, B, xmode, W.invm.p, b, xpre, W.r.p, C.rhs.p, C.e.p, h->Minv.p, gate, rs(), ex());
+        } else {
+            return cycle_tail(l, b, out, gate, br, xmode, xpre);
+        }
+        return cycle_post(l, b, out, gate, br, xmode, xpre, C.e.p, nullptr);
+    }
+
+    bool cycle_tail(int l, const double* b, double* out, const int* gate, const BetaReq* br, int xmode,
+                    const double* xpre) {
+        Level& L = *h->levels[l];
+        LevelWs& W = ws->lev[l];
+        const Csr A = L.csr();
+        const Groups& B = L.groups();
         // r = b - A x ; r_c = restrict(r)
         if (l == 0) mark(0);
         launch_residual(A, B, xmode, W.invm.p, b, xpre, W.r.p, gate, ex());
@@ -212,7 +230,17 @@ struct Plan {
             ec = C.xf.p;
             ec_valid = &ws->fcg.p[l + 1].upd[0];
         }
-        // prolongate + post-smoothing (the last sweep may carry the beta dot)
+        return cycle_post(l, b, out, gate, br, xmode, xpre, ec, ec_valid);
+    }
+
+    // prolongate + post-smoothing (the last sweep may carry the beta dot)
+    bool cycle_post(int l, const double* b, double* out, const int* gate, const BetaReq* br, int xmode,
+                    const double* xpre, const double* ec, const int* ec_valid) {
+        Level& L = *h->levels[l];
+        LevelWs& W = ws->lev[l];
+        const Csr A = L.csr();
+        const Groups& B = L.groups();
+        const bool mat = L.n >= kTmaMinRows;
         const BetaReq* fb = sing() ? nullptr : br;
         if (p.post_sweeps == 0) {
             launch_prolongate(L.n, xmode, W.invm.p, b, xpre, L.v2a.p, ec, ec_valid, out, gate, ex());

@@ -159,7 +159,6 @@ struct Sharded {
     bool cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int beta_state /*0 npcg, 1 fcg l*/);
     void fcg(int l, VRef b, VRef x, GRef parent, bool begun);
     void npcg_iteration(int parity);
-    void xfin_all_sweep_beta(int l, VRef out, GRef g, const VRef* apprev, int beta_state);
 };
 
 bool Sharded::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int beta_state) {

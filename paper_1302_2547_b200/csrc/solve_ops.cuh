@@ -177,6 +177,36 @@ struct EpiResid : NoReduce {
     __device__ void row(int i, double acc, const S&) { r[i] = __dsub_rn(b[i], acc); }
 };
 
+// r = b - A x fused with the restriction into a coarsest level that is ONE
+// aggregate (r_c = sum of r, a deterministic tree instead of the members'
+// order) and its 1x1 solve e_c = Minv r_c (U/solvers.py:146-152; the same
+// value k_dense_solve forms for n = 1)
+struct EpiResidSum {
+    static constexpr int K = 1;
+    const double* b;
+    double* r;
+    const int* g;
+    double* rc;          // coarse right-hand side (1 value)
+    double* ec;          // coarse solution (1 value)
+    const double* minv; // 1x1 coarsest inverse
+    RedSlot<1> red;
+    double s0;
+    __device__ void pre(int i) const { pf(b + i); }
+    __device__ bool gate() const { return g == nullptr || *g; }
+    __device__ void off() {}
+    template <class S>
+    __device__ void row(int i, double acc, const S&) {
+        const double v = __dsub_rn(b[i], acc);
+        r[i] = v;
+        s0 += v;
+    }
+    __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void fin(const double (&t)[1]) {
+        *rc = t[0];
+        *ec = minv[0] * t[0];
+    }
+};
+
 // one sweep: out_i = x_i + invm_i * (b_i - (A x)_i)   (K/numba_backend.py:303-309)
 struct EpiSweep : NoReduce {
     const double* invm;
