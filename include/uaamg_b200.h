@@ -232,6 +232,24 @@ void uaamg_dist_free(uaamg_dist *d);
 int uaamg_gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int *row_ptr, int *col, double *val,
                      int64_t *nnz, void *stream);
 
+/* On-device canonical assembly.
+ * uaamg_from_coo: U/sparse.py:56-74 SparseMatrix.from_coo on device
+ * triplets (int64 rows/cols, float64 vals): stable (row, col) sort,
+ * duplicates summed exactly like np.add.reduceat (a0 + numpy pairwise sum of
+ * the rest), exact zeros dropped; UAAMG_EINVAL on out-of-range coordinates.
+ * uaamg_assemble_laplacian: U/graph.py:63-82 assemble_laplacian on device
+ * edge arrays (ei, ej, w: m edges) and boundary arrays (bj, bw: nb entries),
+ * diagonal weights accumulated in edge-list order.  Both return a
+ * library-owned CSR (int32 row_ptr/col, float64 val on the device). */
+typedef struct uaamg_csr uaamg_csr;
+int uaamg_from_coo(int64_t n_rows, int64_t n_cols, int64_t m, const int64_t *rows, const int64_t *cols,
+                   const double *vals, uaamg_csr **out, void *stream);
+int uaamg_assemble_laplacian(int n, int64_t m, const int64_t *ei, const int64_t *ej, const double *w, int64_t nb,
+                             const int64_t *bj, const double *bw, uaamg_csr **out, void *stream);
+int uaamg_csr_view(const uaamg_csr *c, int *n_rows, int *n_cols, int64_t *nnz, int **row_ptr, int **col,
+                   double **val);
+void uaamg_csr_free(uaamg_csr *c);
+
 /* Row partitions used by the sharded solve (host-only helpers):
  * level 0 in equal 128-row-aligned contiguous blocks; a coarse level by seed
  * ownership (aggregates are numbered by ascending seed, so rank q owns the

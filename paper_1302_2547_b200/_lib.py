@@ -89,6 +89,10 @@ _SIGS = {
     "uaamg_dist_free": (None, [_vp]),
     "uaamg_partition_rows": (_i, [_i, _i, _vp]),
     "uaamg_gen_grid3d": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "uaamg_from_coo": (_i, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp]),
+    "uaamg_assemble_laplacian": (_i, [_i, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
+    "uaamg_csr_view": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "uaamg_csr_free": (None, [_vp]),
     "uaamg_partition_coarse": (_i, [_vp, _i, _vp, _i, _vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),

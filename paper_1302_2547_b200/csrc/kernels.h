@@ -167,6 +167,14 @@ void launch_axpby_init(int n, const double* b, const double* ax, double* r, cuda
 // returns nnz; pass 2 fills col / val
 long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av, cudaStream_t s);
 
+// canonical CSR from device triplets (U/sparse.py:56-74) and the graph
+// Laplacian assembly (U/graph.py:63-82); return nnz, allocate the outputs
+long long device_from_coo(long long nr, long long nc, long long m, const long long* r, const long long* c,
+                          const double* v, DBuf<int>& rp, DBuf<int>& ci, DBuf<double>& av, cudaStream_t s);
+long long device_assemble_laplacian(int n, long long m, const long long* ei, const long long* ej, const double* w,
+                                    long long nb, const long long* bj, const double* bw, DBuf<int>& rp,
+                                    DBuf<int>& ci, DBuf<double>& av, cudaStream_t s);
+
 // ---- setup kernels (kernels_setup.cu) ----
 void launch_degrees(const Csr& A, int* deg, cudaStream_t s);
 void launch_scores(const Csr& A, const int* deg, uint64_t seed, int64_t pass_idx, double* scores, cudaStream_t s);

@@ -70,6 +70,19 @@ def view(address, n, dtype, owner):
     return torch.as_tensor(_CudaView(address, n, dtype, owner), device=cuda_device())
 
 
+class _CsrOwner:
+    """Keeps a library-owned CSR alive while torch views of it exist."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            _lib.load().uaamg_csr_free(self.handle)
+        except Exception:
+            pass
+
+
 class DeviceCSR:
     """Device CSR matrix: int32 row_ptr/col, float64 val (square)."""
 
@@ -90,6 +103,41 @@ class DeviceCSR:
     @classmethod
     def from_arrays(cls, n, row_ptr, col, val):
         return cls(n, n, to_device(row_ptr, np.int32), to_device(col, np.int32), to_device(val, np.float64))
+
+    @classmethod
+    def _from_lib(cls, handle):
+        """Wrap a library-owned uaamg_csr (freed when the last view dies)."""
+        import ctypes
+
+        L = _lib.load()
+        nr, nc, nnz = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        rp, ci, av = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        L.uaamg_csr_view(handle, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nnz), ctypes.byref(rp),
+                         ctypes.byref(ci), ctypes.byref(av))
+        owner = _CsrOwner(handle)
+        return cls(nr.value, nc.value, view(rp.value, nr.value + 1, np.int32, owner),
+                   view(ci.value, nnz.value, np.int32, owner), view(av.value, nnz.value, np.float64, owner))
+
+    @classmethod
+    def from_coo(cls, n_rows, n_cols, rows, cols, vals):
+        """Canonical CSR from triplets on the device: reference
+        SparseMatrix.from_coo (sparse.py:56-74) -- stable (row, col) sort,
+        duplicates summed like np.add.reduceat, exact zeros dropped."""
+        import ctypes
+
+        r = to_device(rows, np.int64)
+        c = to_device(cols, np.int64)
+        v = to_device(vals, np.float64)
+        if not (r.shape == c.shape == v.shape) or r.dim() != 1:
+            raise ValueError("rows, cols and vals must be 1-D of equal length")
+        h = ctypes.c_void_p()
+        rc = _lib.load().uaamg_from_coo(int(n_rows), int(n_cols), int(r.shape[0]), ptr(r), ptr(c), ptr(v),
+                                        ctypes.byref(h), stream())
+        if rc == _lib.UAAMG_EINVAL:
+            from .sparse import SparseFormatError
+            raise SparseFormatError(_lib.last_error())
+        _lib.check(rc)
+        return cls._from_lib(h)
 
     @property
     def nnz(self):
