@@ -9,7 +9,9 @@ there is no CPU fallback.
 
 from .aggregation import (Aggregation, AggregationConfig, AggregationError, aggregate, compose,
                           quasi_random_scores, select_coarse_vertices, singleton_aggregation)
+from .analysis import TwoLevelReport, hierarchy_report, q_energy_norm, reports_to_csv, two_level_rate
 from .device import DeviceCSR
+from .graph import GraphError, GraphProblem, assemble_laplacian, assemble_laplacian_device, generate_structured_grid
 from .hierarchy import CoarseSolver, Hierarchy, Level, SetupError, detect_singular, galerkin_coarse, setup
 from .solvers import (CycleSpec, NumericalError, Smoother, SolveReport, cycle, npcg_solve, prolongate_add,
                       restrict, smooth, smoother_inverse_diag)
@@ -24,5 +26,7 @@ __all__ = [
     "CycleSpec", "NumericalError", "Smoother", "SolveReport", "cycle", "npcg_solve", "prolongate_add", "restrict",
     "smooth", "smoother_inverse_diag",
     "SparseMatrix", "SparseFormatError", "DeviceCSR",
+    "TwoLevelReport", "hierarchy_report", "q_energy_norm", "reports_to_csv", "two_level_rate",
+    "GraphError", "GraphProblem", "assemble_laplacian", "assemble_laplacian_device", "generate_structured_grid",
     "__version__",
 ]

@@ -87,3 +87,18 @@ def test_grid2d_through_device_assembly_solves_like_host(U):
     bj = v[miss > 0]
     d = assemble_laplacian_device(n * n, (ei, ej, np.ones(ei.size)), (bj, miss[miss > 0]))
     _eq(d, A.indptr, A.indices, A.data)
+
+
+@pytest.mark.parametrize("n,bc,aniso", [(31, "dirichlet", (1.0, 1.0)), (24, "dirichlet", (0.3, 1.7)),
+                                        (20, "neumann", (1.0, 0.1))])
+def test_reference_api_grid_problem(U, n, bc, aniso):
+    """generate_structured_grid + assemble_laplacian (device assembly) ==
+    the host builder (itself pinned to the reference's assembly)."""
+    from paper_1302_2547_b200 import problems
+
+    P = U.generate_structured_grid(n, bc, aniso)
+    A = U.assemble_laplacian(P)
+    B = problems.grid2d(n, bc, aniso)
+    assert np.array_equal(A.indptr, B.indptr) and np.array_equal(A.indices, B.indices)
+    assert np.array_equal(A.data, B.data)
+    assert P.singular == (bc == "neumann")
