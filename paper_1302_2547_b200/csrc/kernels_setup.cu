@@ -398,6 +398,26 @@ __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int tid, int nth, in
     }
 }
 
+// append every k in [0, n) with flag[k] == stamp to list, in vertex order
+// within each warp (one atomic per warp)
+__device__ __forceinline__ void wl_append(bool f, int k, int* list, int* cnt) {
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    int b = 0;
+    if (lane == 0) b = atomicAdd(cnt, __popc(m));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (f) list[b + __popc(m & ((1u << lane) - 1u))] = k;
+}
+__device__ void wl_compact(const int* mark, int stamp, int n, int* list, int* cnt, int tid, int nth) {
+    const int n32 = (n + 31) & ~31;  // whole warps iterate together
+    for (int k = tid; k < n32; k += nth) wl_append(k < n && mark[k] == stamp, k, list, cnt);
+}
+__device__ void wl_compact_st(const uint8_t* st, int n, int* list, int* cnt, int tid, int nth) {
+    const int n32 = (n + 31) & ~31;
+    for (int k = tid; k < n32; k += nth) wl_append(k < n && st[k] == 0, k, list, cnt);
+}
+
 __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
     cg::grid_group grid = cg::this_grid();
     const Csr& A = g.A;
@@ -424,7 +444,8 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             g.prof[4 * pass + 1] = U.cnt;
         }
         const int itg0 = itg;
-        // scores of U (K/numba_backend.py:100-111); H = U and its neighbours
+        // scores of U (K/numba_backend.py:100-111); mark H = U and its
+        // neighbours (plain stores), then compact H in vertex order
         const uint64_t base = pass_base(g.seed, pass);
         const int stamp = pass + 1;
         int* hcnt = (int*)&ctl[14 + (pass & 1)];
@@ -432,14 +453,17 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             const int i = U[t];
             const double u = hash_unit(base, i);
             g.sc[i] = __dadd_rn((double)g.deg[i], __ddiv_rn(__dadd_rn((double)(i % 12), u), 12.0));
-            if (U.list)
-                for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
-                    const int k = __ldg(A.ci + e);
-                    if (atomicExch(g.mark + k, stamp) != stamp) g.hlist[atomicAdd(hcnt, 1)] = k;
-                }
+            if (U.list) {
+                g.mark[i] = stamp;
+                for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) g.mark[__ldg(A.ci + e)] = stamp;
+            }
         }
         grid.sync();
-        if (U.list) H = WL{g.hlist, ctl[14 + (pass & 1)]};
+        if (U.list) {
+            wl_compact(g.mark, stamp, n, g.hlist, hcnt, tid, nth);
+            grid.sync();
+            H = WL{g.hlist, ctl[14 + (pass & 1)]};
+        }
         coop_hop1(g, H, 0, tid, nth, lane, w, nw);
         grid.sync();
         // selection (K/numba_backend.py:175-193)
@@ -527,17 +551,21 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             if (!any) break;
         }
         // commit: admitted vertices and centers are processed, seeded by
-        // owner; the rest form the next pass's U
+        // owner; the rest form the next pass's U (compacted in vertex order)
         int left = 0;
         int* ucnt = (int*)&ctl[11 + ps];
         for (int t = tid; t < U.cnt; t += nth) {
             const int j = U[t];
             const uint8_t sj = g.st[j];
             if (sj == 1 || (sj == 0 && adm[j])) { g.seed_of[j] = g.owner[j]; g.st[j] = 2; }
-            else if (sj == 0) { ++left; unext[atomicAdd(ucnt, 1)] = j; }
+            else if (sj == 0) ++left;
         }
         if (left) atomicAdd((int*)&ctl[3 + ps], left);
         grid.sync();
+        if (ctl[3 + ps] > 0) {
+            wl_compact_st(g.st, n, unext, ucnt, tid, nth);
+            grid.sync();
+        }
         if (g.prof && tid == 0 && pass < 32) {
             g.prof[4 * pass + 2] = H.cnt;
             g.prof[4 * pass + 3] = itg - itg0;
