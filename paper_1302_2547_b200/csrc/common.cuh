@@ -61,6 +61,28 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
         ::uaamg::g_launches.fetch_add(1, std::memory_order_relaxed);                            \
     } while (0)
 
+// Generation barrier over a co-resident (cooperatively launched) grid:
+// bar[0] arrivals (back to 0 after each barrier), bar[1] generation.
+__device__ __noinline__ inline void coop_grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            const long long t0 = clock64();
+            while (*gen == g)
+                if (clock64() - t0 > (1ll << 34)) __trap();  // a lost CTA: fail loudly
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------- device memory
 // Stream-ordered allocation from the device's default memory pool.
 template <class T>

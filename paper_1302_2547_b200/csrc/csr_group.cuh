@@ -159,4 +159,69 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, S
     }
 }
 
+// Flexible-CG direction SpMV fused with the update that consumes it
+// (U/solvers.py:173-185): phase 1 is k_csr_group's direction + Ap + p.Ap,
+// p.r; a grid barrier; every CTA folds the per-CTA partials in block order
+// (same bits everywhere) and, unless p'Ap <= 0 (break), applies
+// x += alpha p, r = r_in - alpha Ap on a grid-stride range and reduces ||r||
+// through the ticketed last-block finish.  One cooperative launch instead of
+// two dependent kernels; same arithmetic per element.
+template <class Src>
+__global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, Src src_p, EpiDirFcg epi_p,
+                                                              BodyFcgUpd upd_p, double* part, unsigned* bar) {
+    __shared__ double win[kGrpWarps][kGrpRound];
+    __shared__ double sm[kThreads / 32 + 1];
+    __shared__ double tot[2];
+    pdl_wait();
+    pdl_trigger();
+    EpiDirFcg epi = epi_p;
+    if (!epi.gate()) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            epi.off();
+            upd_p.off();
+        }
+        return;
+    }
+    Src src = src_p;
+    src.init();
+    const int nu = G.units();
+    for (int u = blockIdx.x * kGrpWarps + (threadIdx.x >> 5); u < nu; u += gridDim.x * kGrpWarps)
+        grp_unit<false>(A, G, u, src, epi, win[threadIdx.x >> 5]);
+    double v[2];
+    epi.vals(v);
+    const double b0 = block_sum<kThreads>(v[0], sm);
+    const double b1 = block_sum<kThreads>(v[1], sm);
+    const int nb = gridDim.x;
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = b0;
+        part[nb + blockIdx.x] = b1;
+    }
+    coop_grid_sync(bar);
+    if (threadIdx.x < 32) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int b = threadIdx.x; b < nb; b += 32) {
+            t0 += __ldcg(part + b);
+            t1 += __ldcg(part + nb + b);
+        }
+        t0 = warp_sum(t0);
+        t1 = warp_sum(t1);
+        if (threadIdx.x == 0) {
+            tot[0] = t0;
+            tot[1] = t1;
+        }
+    }
+    __syncthreads();
+    const double t[2] = {tot[0], tot[1]};
+    if (blockIdx.x == 0 && threadIdx.x == 0) epi.fin(t);  // pap, pr, upd[step], alpha for later readers
+    if (!(t[0] > 0.0)) {  // breakdown: the update is gated off (U/solvers.py:179-180)
+        if (blockIdx.x == 0 && threadIdx.x == 0) upd_p.off();
+        return;
+    }
+    BodyFcgUpd upd = upd_p;
+    upd.alpha = t[1] / t[0];
+    double s[1] = {0.0};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) upd.item(i, s);
+    grid_reduce_finish<1>(s, upd.red.partials, upd.red.ticket, [&](const double (&tt)[1]) { upd.fin(tt); });
+}
+
 }  // namespace uaamg

@@ -129,6 +129,12 @@ void launch_restrict(int nc, const int* agg_ptr, const int* members, const Group
 void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                     const double* r, double* p, double* ap, FcgState* st, int step, RedScratch rs,
                     Exec ex);
+// fused direction SpMV + update of one flexible-CG step on a small level (one
+// cooperative launch; falls back to the two kernels when recording or on TMA
+// levels).  bar: 2 zeroed unsigned, part: >= 2 * kNumSMs * 8 doubles
+void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
+                           const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
+                           RedScratch rs, double* part, unsigned* bar, Exec ex);
 // NPCG flavour (have_prev / breakdown handled on device)
 void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);

@@ -124,6 +124,43 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
     run_stream<SrcDir, EpiDirFcg, false>(A, G, src, e, ex);
 }
 
+void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
+                           const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
+                           RedScratch rs, double* part, unsigned* bar, Exec ex) {
+    if (ex.rec || G.tma_cap > 0) {
+        launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
+        launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex);
+        return;
+    }
+    EpiDirFcg e{};
+    e.p = p; e.ap = ap; e.r = r; e.st = st; e.step = step; e.red = {rs.partials, rs.ticket};
+    SrcDir src{};
+    src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = nullptr; src.have_static = have_prev;
+    BodyFcgUpd u{};
+    u.step = step; u.x = x; u.p = p; u.rin = r; u.rout = r_out; u.ap = ap; u.st = st; u.singular = 0;
+    u.red = {rs.partials, rs.ticket};
+    static int maxg = 0;
+    if (!maxg) {
+        int occ = 0;
+        UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dir_update<SrcDir>, 32 * kGrpWarps, 0));
+        maxg = std::max(1, occ) * kNumSMs;
+    }
+    const int grid = std::max(1, std::min(cdiv(std::max(G.units(), 1), kGrpWarps), std::min(maxg, kNumSMs * 8)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32 * kGrpWarps);
+    cfg.stream = ex.s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    UA_CK(cudaLaunchKernelEx(&cfg, k_dir_update<SrcDir>, A, G, src, e, u, part, bar));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s) {
     EpiDirNpcg e{};

@@ -257,6 +257,9 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
     ws->err.alloc(1, s);
     UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
     ws->bad_row.alloc(1, s);
+    ws->fpart.alloc(2 * (size_t)kNumSMs * 8, s);
+    ws->fbar.alloc(2, s);
+    UA_CK(cudaMemsetAsync(ws->fbar.p, 0, 2 * sizeof(unsigned), s));
     const bool sing = h->singular;
     for (int l = 0; l < nl; ++l) {
         Level& L = *h->levels[l];

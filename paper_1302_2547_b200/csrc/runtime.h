@@ -67,6 +67,8 @@ struct SolveWs {
     int prof_runs = 0;
     DBuf<double> epart;
     DBuf<unsigned> ebar;
+    DBuf<double> fpart;    // fused direction + update: per-CTA partials
+    DBuf<unsigned> fbar;   // and its grid barrier
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     uint64_t graph_kernels[2] = {0, 0};  // kernel launches recorded per graph
     // level-0 hot-kernel timing (profile_level0): event pairs per graph parity
@@ -304,8 +306,13 @@ struct Plan {
             const BetaReq br{app, &st->beta, &st->pap, nullptr};
             const bool fused = cycle(l, rin, W.z.p, g, k > 0 ? &br : nullptr);
             if (k > 0 && !fused) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
-            launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
-            launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
+            if (!sing()) {
+                launch_dir_update_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, x, W.rf.p, st, k, rs(),
+                                      ws->fpart.p, ws->fbar.p, ex());
+            } else {
+                launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
+                launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
+            }
         }
     }
 
