@@ -29,9 +29,11 @@ __global__ void __launch_bounds__(kThreads) k_map(int n, Body body_p) {
     }
 }
 
+// elementwise maps are latency-bound per thread (3-5 independent loads per
+// item): up to 8 resident CTAs per SM, ~2 items per thread on large levels
 inline int map_grid(int n) {
-    int g = cdiv(n, kThreads * 4);
-    return g < 1 ? 1 : (g > 2 * kNumSMs ? 2 * kNumSMs : g);
+    int g = cdiv(n, kThreads * 2);
+    return g < 1 ? 1 : (g > 8 * kNumSMs ? 8 * kNumSMs : g);
 }
 
 template <class Body>
