@@ -247,3 +247,14 @@ def test_device_grid_generator_matches_host(U, dims, stencil, bc):
     d = problems.grid3d_device(None, stencil, bc, dims=dims).to_host()
     assert np.array_equal(h.indptr, d.indptr) and np.array_equal(h.indices, d.indices)
     assert np.array_equal(h.data, d.data)
+
+
+@pytest.mark.parametrize("case", ["g3d7_16", "c1_grid2d_256", "rgg_20000", "g2d_dir_64_t5"])
+def test_persistent_engine_matches_reference(U, case):
+    """The persistent coarse engine (csrc/engine.cu, off by default) runs the
+    recorded K-cycle ops of every level below a threshold in one cooperative
+    launch; its histories must meet the same bar as the launch path."""
+    h, g, ip = _setup(U, case)
+    b = g["b"] if g["b"].shape[0] else np.ones(ip.shape[0] - 1)
+    x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500, engine_rows=20000)
+    assert_history_close(rep.residual_history, g, rtol=RTOL)
