@@ -50,6 +50,13 @@ def dist_init():
     import torch.distributed as dist
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if os.environ.get("BENCH_SAME_DEVICE"):
+        # functional check of the multi-process path on a one-GPU box: every
+        # rank on device 0, gloo for the host-side collectives
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return rank, ws, local
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, ws, local
@@ -428,16 +435,62 @@ def run_ours(args, rank, ws, local):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, ws, local):
+    """--mode sharded: the row-partitioned multi-GPU solve (csrc/shard.cu via
+    npcg_solve_distributed), weak-scaled on the north star's per-GPU share
+    of C5 -- every rank owns a 512 x 512 x 64 slab of a 512 x 512 x (64 N)
+    7-point box.  The hierarchy is built on every rank (setup is replicated,
+    DESIGN.md section 6); value = max over ranks of setup + sharded solve."""
+    import torch
+    import torch.distributed as dist
+    import paper_1302_2547_b200 as U
+    from paper_1302_2547_b200 import problems
+    from paper_1302_2547_b200.distributed import npcg_solve_distributed
+
+    dev = torch.device("cuda", local)
+    nz = int(os.environ.get("BENCH_SLAB_Z", "64"))
+    A = problems.grid3d_device(None, 7, dims=(nz * ws, 512, 512))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device=dev)
+    times, its = [], 0
+    for k in range(max(args.warmup, 1) + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = U.setup(A)
+        x, rep = npcg_solve_distributed(h, U.CycleSpec(), U.Smoother(), b, tol=TOL, max_iters=500)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        its = rep.iterations
+        del h
+        if k >= max(args.warmup, 1):
+            times.append(dt)
+    t = torch.tensor([float(np.mean(times))], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": float(t.item()), "unit": "s", "n_gpus": ws, "steps": args.steps,
+                          "warmup": max(args.warmup, 1), "ms_per_step": float(t.item()) * 1e3,
+                          "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1, x0 = 0)",
+                          "config": {"workload": f"sharded solve, 7-point box {A.n_rows} unknowns "
+                                                 f"({ws} ranks x one C5 slab each)", "iterations": int(its),
+                                     "parallelism": f"row-partitioned x{ws} (IPC peer gathers)",
+                                     "timing": "wall clock, max over ranks"}}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="N > 1: independent C2 replicas (default) or the row-partitioned solve")
     args = ap.parse_args()
     rank, ws, local = dist_init()
     if args.impl == "reference":
         run_reference(args, rank, ws)
+    elif args.mode == "sharded" and ws > 1:
+        run_sharded(args, rank, ws, local)
     else:
         run_ours(args, rank, ws, local)
     if ws > 1:
