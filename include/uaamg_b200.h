@@ -264,6 +264,12 @@ int uaamg_partition_coarse(const int *seeds, int nc, const int *fine_bounds, int
  * [2] direction SpMV (+ dots).  *count = iterations timed. */
 int uaamg_solve_profile(const uaamg_hierarchy *h, double *seconds3, double *bytes3, int64_t *count);
 
+/* Which level the last solve ran as one thread-block cluster (the coarse
+ * tail kernel: the level above the coarsest, with its coarsest solve); -1
+ * when the separate-kernel path ran.  *cluster = CTAs in that cluster.
+ * (Diagnostics; UAAMG_NO_TAIL=1 in the environment disables the tail.) */
+int uaamg_tail_info(const uaamg_hierarchy *h, int *level, int *cluster);
+
 /* U/solvers.py:128-157: one cycle on level `level` from a zero guess. */
 int uaamg_cycle(uaamg_hierarchy *h, const uaamg_solve_params *p, int level, const double *b, double *x,
                 void *stream);

@@ -69,8 +69,18 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
                 for (int q = 0; q < kGrpU; ++q) win[lane + 32 * q] = Unit ? v[q] : __dmul_rn(a[q], v[q]);
                 __syncwarp();
                 if (mine) {
-                    const int l0 = max(bi, base), l1 = min(ei, base + kGrpRound);
-                    for (int e = l0; e < l1; ++e) acc = __dadd_rn(acc, win[e - base]);
+                    // sequential in k; window reads batched 8 at a time so
+                    // only the DADD chain is serial, not LDS -> DADD
+                    const int l1 = min(ei, base + kGrpRound) - base;
+                    int e = max(bi, base) - base;
+                    for (; e + 8 <= l1; e += 8) {
+                        double w[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) w[q] = win[e + q];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, w[q]);
+                    }
+                    for (; e < l1; ++e) acc = __dadd_rn(acc, win[e]);
                 }
                 __syncwarp();
             }
@@ -107,9 +117,12 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
             __threadfence();
+            // all partials loaded at once (lane k: pieces k, k+32, ...), then a
+            // fixed-shape warp tree: one L2 round trip instead of np
+            double acc = 0.0;
+            for (int k = lane; k < np; k += 32) acc = __dadd_rn(acc, __ldcg(G.part + p0 + k));
+            acc = warp_sum(acc);
             if (lane == 0) {
-                double acc = 0.0;
-                for (int k = 0; k < np; ++k) acc = __dadd_rn(acc, __ldcg(G.part + p0 + k));
                 G.ticket[lr] = 0u;
                 epi.row(row, acc, src);
             }

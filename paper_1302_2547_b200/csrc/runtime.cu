@@ -334,6 +334,37 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         UA_CK(cudaMemsetAsync(ws->ebar.p, 0, 2 * sizeof(unsigned), s));
         UA_CK(cudaStreamSynchronize(s));  // ops vector is a host temporary
     }
+    // the level above the coarsest as one cluster kernel (tail.cu)
+    if (!getenv("UAAMG_NO_TAIL") && ws->Lc < 0 && !sing && nl >= 3 && p.pre_sweeps <= 1 && p.post_sweeps <= 1) {
+        const int Lt = nl - 2;
+        const Level& T = *h->levels[Lt];
+        const Level& U = *h->levels[Lt - 1];
+        auto d2h = [&](auto* dp, size_t count) {
+            std::vector<std::remove_const_t<std::remove_pointer_t<decltype(dp)>>> v(count);
+            if (count) UA_CK(cudaMemcpyAsync(v.data(), dp, sizeof(v[0]) * count, cudaMemcpyDeviceToHost, s));
+            return v;
+        };
+        TailInputs in;
+        in.n = T.n;
+        in.rp = d2h(T.rp.p, T.n + 1);
+        in.ci = d2h(T.ci.p, T.nnz);
+        in.av = d2h(T.av.p, T.nnz);
+        in.invm = d2h(ws->lev[Lt].invm.p, T.n);
+        in.mp = d2h(U.agg_ptr.p, U.nc + 1);
+        in.mem = d2h(U.members.p, U.n);
+        in.nc = h->levels[nl - 1]->n;
+        if (in.nc > 1) {
+            in.v2a = d2h(T.v2a.p, T.n);
+            in.cp = d2h(T.agg_ptr.p, T.nc + 1);
+            in.cmem = d2h(T.members.p, T.n);
+        }
+        in.minv = d2h(h->Minv.p, (size_t)in.nc * in.nc);
+        UA_CK(cudaStreamSynchronize(s));
+        in.pre = p.pre_sweeps;
+        in.post = p.post_sweeps;
+        in.steps = (!p.kcycle || p.inner_krylov_steps == 0) ? 0 : p.inner_krylov_steps;
+        if (build_tail(in, ws->tail, s)) ws->tail.Lt = Lt;
+    }
     ws->ready = true;
     UA_CK(cudaStreamSynchronize(s));
     return ws;
@@ -490,6 +521,7 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     UA_CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    print_tail_prof(ws->tail);
     if (ws->eprof.p && ws->neops > 0) {
         // diagnostics: per-op durations of the last engine run, by (kind, rows)
         std::vector<unsigned long long> t(ws->neops + 1);
@@ -626,6 +658,15 @@ int uaamg_solve_profile(const uaamg_hierarchy* h, double* seconds3, double* byte
         bytes3[2] = csr + 40.0 * n;             // direction SpMV: z, p_prev, r in; p, Ap out
         for (int k = 0; k < 3; ++k) seconds3[k] = h->ws->prof_seconds[k];
         *count = h->ws->prof_count;
+    })
+}
+
+int uaamg_tail_info(const uaamg_hierarchy* h, int* level, int* cluster) {
+    UA_GUARD({
+        if (!h->ws) throw Error(UAAMG_EINVAL, "no solve has run on this hierarchy");
+        const bool on = h->ws->tail.on;
+        *level = on ? h->ws->tail.Lt : -1;
+        *cluster = on ? h->ws->tail.args.cs : 0;
     })
 }
 

@@ -16,6 +16,7 @@
 #include "csr_tma.cuh"
 #include "engine.h"
 #include "setup.h"
+#include "tail.h"
 
 namespace uaamg {
 
@@ -67,6 +68,7 @@ struct SolveWs {
     int prof_runs = 0;
     DBuf<double> epart;
     DBuf<unsigned> ebar;
+    TailPlan tail;         // the level above the coarsest in one cluster (tail.cu)
     DBuf<double> fpart;    // fused direction + update: per-CTA partials
     DBuf<unsigned> fbar;   // and its grid barrier
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -215,12 +217,23 @@ struct Plan {
         const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
         // the coarse flexible CG's ||r_c|| / gate[0] come out of the restriction
         const bool begun = !direct && !sing();
-        launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex(),
-                        begun ? ws->fcg.p + l + 1 : nullptr, rs());
-        if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
+        // the tail kernel restricts, solves and returns the coarse correction
+        const bool tail = ws->tail.on && l + 1 == ws->tail.Lt && rec == nullptr;
+        if (!tail) {
+            launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex(),
+                            begun ? ws->fcg.p + l + 1 : nullptr, rs());
+            if (sing()) launch_project_mean(L.nc, C.rhs.p, ws->sums.p + 4 * l + 1, gate, rs(), ex());
+        }
         const double* ec;
         const int* ec_valid = nullptr;
-        if (l + 1 == ws->Lc) {
+        if (tail) {
+            double* o = direct ? C.e.p : C.xf.p;
+            int* u0 = direct ? nullptr : &ws->fcg.p[l + 1].upd[0];
+            launch_tail(ws->tail, W.r.p, gate, o, u0, s);
+            if (getenv("UAAMG_TAIL_TWICE")) launch_tail(ws->tail, W.r.p, gate, o, u0, s);
+            ec = o;
+            ec_valid = u0;
+        } else if (l + 1 == ws->Lc) {
             engine(gate);
             ec = direct ? C.e.p : C.xf.p;
             if (!direct) ec_valid = &ws->fcg.p[l + 1].upd[0];
