@@ -311,9 +311,13 @@ __global__ void k_capped_commit(int n, uint8_t* st, uint8_t* newly, int* remaini
 // bit-identical to the full sweeps.  Processed vertices keep stale
 // owner/adm values; they cannot match a current center (centers are
 // unprocessed until their own commit).  Short rows are handled
-// thread-per-item, rows longer than kLongRow warp-per-item.
+// thread-per-item, rows longer than kLongRow warp-per-item from a list of
+// the level's long rows (built once; membership in U / H is checked per
+// item), so the warp loops cost nothing on levels without long rows.
 struct AggCoop {
     Csr A;
+    const int* longs;     // rows longer than kLongRow (any order)
+    const int* nlongs;    // their count (device)
     const int* deg;
     uint64_t seed;
     int max_passes;
@@ -362,7 +366,8 @@ struct WL {
 
 // hop1 over the items of H: max key over the row's unprocessed (mode 0) or
 // center (mode 1) neighbours
-__device__ void coop_hop1(const AggCoop& g, WL H, int mode, int tid, int nth, int lane, int w, int nw) {
+__device__ void coop_hop1(const AggCoop& g, WL H, int mode, int stamp, int nlong, int tid, int nth, int lane, int w,
+                          int nw) {
     const Csr& A = g.A;
     for (int t = tid; t < H.cnt; t += nth) {
         const int k = H[t];
@@ -380,10 +385,10 @@ __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int tid, int nth, in
         g.ms[k] = bs;
         g.mi[k] = bi;
     }
-    for (int t = w; t < H.cnt; t += nw) {
-        const int k = H[t];
+    for (int t = w; t < nlong; t += nw) {
+        const int k = g.longs[t];
+        if (H.list && g.mark[k] != stamp) continue;  // not in H
         const int e0 = A.rp[k], e1 = A.rp[k + 1];
-        if (e1 - e0 <= kLongRow) continue;
         double bs = 0.0;
         int bi = -1;
         for (int e = e0 + lane; e < e1; e += 32) {
@@ -418,6 +423,12 @@ __device__ void wl_compact_st(const uint8_t* st, int n, int* list, int* cnt, int
     for (int k = tid; k < n32; k += nth) wl_append(k < n && st[k] == 0, k, list, cnt);
 }
 
+// rows longer than kLongRow, appended in any order
+__global__ void k_long_rows(Csr A, int* list, int* cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x)
+        if (A.rp[i + 1] - A.rp[i] > kLongRow) list[atomicAdd(cnt, 1)] = i;
+}
+
 __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
     cg::grid_group grid = cg::this_grid();
     const Csr& A = g.A;
@@ -426,6 +437,7 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
     const int lane = threadIdx.x & 31, w = tid >> 5, nw = nth >> 5;
     volatile int* ctl = g.ctl;
     int remaining = n, pass = 0, itg = 0;
+    const int nlong = *g.nlongs;
     WL U{nullptr, n}, H{nullptr, n};
     for (; pass < g.max_passes; ++pass) {
         if (remaining == 0) break;  // U/aggregation.py:186
@@ -464,7 +476,7 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             grid.sync();
             H = WL{g.hlist, ctl[14 + (pass & 1)]};
         }
-        coop_hop1(g, H, 0, tid, nth, lane, w, nw);
+        coop_hop1(g, H, 0, stamp, nlong, tid, nth, lane, w, nw);
         grid.sync();
         // selection (K/numba_backend.py:175-193)
         int local = 0;
@@ -477,10 +489,10 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             row_hopmax(A, g.ms, g.mi, i, e0, e1, 1, bs, bi);
             if (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi)) { g.st[i] = 1; ++local; }
         }
-        for (int t = w; t < U.cnt; t += nw) {
-            const int i = U[t];
+        for (int t = w; t < nlong; t += nw) {
+            const int i = g.longs[t];
+            if (g.st[i] != 0) continue;  // in U and not yet a center
             const int e0 = A.rp[i], e1 = A.rp[i + 1];
-            if (e1 - e0 <= kLongRow || g.st[i] != 0) continue;
             double bs = 0.0;
             int bi = -1;
             row_hopmax(A, g.ms, g.mi, i, e0 + lane, e1, 32, bs, bi);
@@ -489,7 +501,7 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
         }
         if (local) atomicAdd((int*)&ctl[ps], local);
         grid.sync();
-        coop_hop1(g, H, 1, tid, nth, lane, w, nw);
+        coop_hop1(g, H, 1, stamp, nlong, tid, nth, lane, w, nw);
         grid.sync();
         // claim (K/numba_backend.py:196-220) + admission seeds
         for (int t = tid; t < U.cnt; t += nth) {
@@ -505,10 +517,10 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
             row_hopmax(A, g.ms, g.mi, j, e0, e1, 1, bs, bi);
             g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
         }
-        for (int t = w; t < U.cnt; t += nw) {
-            const int j = U[t];
+        for (int t = w; t < nlong; t += nw) {
+            const int j = g.longs[t];
+            if (g.st[j] != 0) continue;
             const int e0 = A.rp[j], e1 = A.rp[j + 1];
-            if (e1 - e0 <= kLongRow || g.st[j] != 0) continue;
             double bs = 0.0;
             int bi = -1;
             row_hopmax(A, g.ms, g.mi, j, e0 + lane, e1, 32, bs, bi);
@@ -532,11 +544,12 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
                     if (adm[nb] && g.owner[nb] == c) { adm[j] = 1; ch = 1; break; }
                 }
             }
-            for (int t = w; t < U.cnt; t += nw) {
-                const int j = U[t];
+            for (int t = w; t < nlong; t += nw) {
+                const int j = g.longs[t];
+                if (g.st[j] == 2) continue;  // processed: not in U
                 const int c = g.owner[j];
                 const int e0 = A.rp[j], e1 = A.rp[j + 1];
-                if (c < 0 || c == j || adm[j] || e1 - e0 <= kLongRow) continue;
+                if (c < 0 || c == j || adm[j]) continue;
                 bool f = false;
                 for (int e = e0 + lane; e < e1 && !f; e += 32) {
                     const int nb = __ldg(A.ci + e);
@@ -1013,12 +1026,16 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
     int passes = 0;
     int remaining = n;
     if (!capped) {
-        DBuf<int> ctl(16, s);
+        DBuf<int> ctl(17, s);
         SPtr<int> ul0{scratch<int>(9, n)}, ul1{scratch<int>(10, n)}, hl{scratch<int>(11, n)}, mark{scratch<int>(12, n)};
-        UA_CK(cudaMemsetAsync(ctl.p, 0, 16 * sizeof(int), s));
+        UA_CK(cudaMemsetAsync(ctl.p, 0, 17 * sizeof(int), s));
         UA_CK(cudaMemsetAsync(mark.p, 0, sizeof(int) * n, s));
+        SPtr<int> longs{scratch<int>(13, n)};
+        UA_LAUNCH(k_long_rows, std::min(cdiv(n, 256), 4 * 148), 256, 0, s, A, longs.p, ctl.p + 16);
         AggCoop g;
-        g.A = A; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
+        g.A = A;
+        g.longs = longs.p;
+        g.nlongs = ctl.p + 16; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
         g.mi = mi.p; g.owner = owner.p; g.adm = adm.p; g.seed_of = seed_of.p; g.ctl = ctl.p;
         g.ulist[0] = ul0.p; g.ulist[1] = ul1.p; g.hlist = hl.p; g.mark = mark.p;
         static const bool aprof = getenv("UAAMG_AGG_PROF") != nullptr;
