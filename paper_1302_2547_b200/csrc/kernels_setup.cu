@@ -345,15 +345,42 @@ __device__ __forceinline__ void warp_keymax(double& s, int& i) {
     }
 }
 
-// max key over row r of the hop-1 table (ms, mi); lanes split the row when warp
+// max key over row r of the hop-1 table (ms, mi); lanes split the row when
+// warp (step 32: four strided entries per lane in flight -- the key order is
+// total, so the maximum does not depend on the visiting order)
 __device__ __forceinline__ void row_hopmax(const Csr& A, const double* ms, const int* mi, int r, int e0, int e1,
                                            int step, double& bs, int& bi) {
-    for (int e = e0; e < e1; e += step) {
-        const int k = __ldg(A.ci + e);
-        const int c = mi[k];
-        if (c < 0) continue;
-        const double v = ms[k];
-        if (bi < 0 || key_gt(v, c, bs, bi)) { bs = v; bi = c; }
+    if (step == 1) {
+        // one thread: 8 entries in flight per batch
+        for (int e = e0; e < e1; e += 8) {
+            int k[8], c[8];
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) k[q] = e + q < e1 ? __ldg(A.ci + e + q) : -1;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = k[q] >= 0 ? mi[k[q]] : -1;
+                v[q] = k[q] >= 0 ? ms[k[q]] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (c[q] >= 0 && (bi < 0 || key_gt(v[q], c[q], bs, bi))) { bs = v[q]; bi = c[q]; }
+        }
+        return;
+    }
+    for (int e = e0; e < e1; e += 4 * step) {
+        int k[4], c[4];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) k[q] = e + q * step < e1 ? __ldg(A.ci + e + q * step) : -1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c[q] = k[q] >= 0 ? mi[k[q]] : -1;
+            v[q] = k[q] >= 0 ? ms[k[q]] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (c[q] >= 0 && (bi < 0 || key_gt(v[q], c[q], bs, bi))) { bs = v[q]; bi = c[q]; }
     }
 }
 
@@ -375,12 +402,22 @@ __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int stamp, int nlong
         if (e1 - e0 > kLongRow) continue;
         double bs = 0.0;
         int bi = -1;
-        for (int e = e0; e < e1; ++e) {
-            const int j = __ldg(A.ci + e);
-            const uint8_t sj = g.st[j];
-            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
-            const double v = g.sc[j];
-            if (bi < 0 || key_gt(v, j, bs, bi)) { bs = v; bi = j; }
+        for (int e = e0; e < e1; e += 8) {
+            int j[8];
+            uint8_t sj[8];
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) j[q] = e + q < e1 ? __ldg(A.ci + e + q) : -1;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sj[q] = j[q] >= 0 ? g.st[j[q]] : (mode == 0 ? 2 : 0);  // padding: skipped
+                v[q] = j[q] >= 0 ? g.sc[j[q]] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (mode == 0 ? (sj[q] == 2) : (sj[q] != 1)) continue;
+                if (bi < 0 || key_gt(v[q], j[q], bs, bi)) { bs = v[q]; bi = j[q]; }
+            }
         }
         g.ms[k] = bs;
         g.mi[k] = bi;
@@ -391,12 +428,22 @@ __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int stamp, int nlong
         const int e0 = A.rp[k], e1 = A.rp[k + 1];
         double bs = 0.0;
         int bi = -1;
-        for (int e = e0 + lane; e < e1; e += 32) {
-            const int j = __ldg(A.ci + e);
-            const uint8_t sj = g.st[j];
-            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
-            const double v = g.sc[j];
-            if (bi < 0 || key_gt(v, j, bs, bi)) { bs = v; bi = j; }
+        for (int e = e0 + lane; e < e1; e += 128) {
+            int j[4];
+            uint8_t sj[4];
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) j[q] = e + 32 * q < e1 ? __ldg(A.ci + e + 32 * q) : -1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                sj[q] = j[q] >= 0 ? g.st[j[q]] : (mode == 0 ? 2 : 0);  // padding: skipped
+                v[q] = j[q] >= 0 ? g.sc[j[q]] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (mode == 0 ? (sj[q] == 2) : (sj[q] != 1)) continue;
+                if (bi < 0 || key_gt(v[q], j[q], bs, bi)) { bs = v[q]; bi = j[q]; }
+            }
         }
         warp_keymax(bs, bi);
         if (lane == 0) { g.ms[k] = bs; g.mi[k] = bi; }
@@ -429,8 +476,25 @@ __global__ void k_long_rows(Csr A, int* list, int* cnt) {
         if (A.rp[i + 1] - A.rp[i] > kLongRow) list[atomicAdd(cnt, 1)] = i;
 }
 
-__global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
-    cg::grid_group grid = cg::this_grid();
+// barrier between phases: the whole cooperative grid, or -- small levels --
+// one thread-block cluster (hardware barrier, release/acquire at cluster
+// scope; the acquire invalidates L1, so plain loads see the other CTAs'
+// global writes)
+struct GridBar {
+    __device__ void sync() const { cg::this_grid().sync(); }
+};
+struct ClusterBar {
+    __device__ void sync() const {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+};
+constexpr int kAggClusterThreads = 512;
+constexpr int kAggClusterCtas = 16;
+constexpr int kAggClusterMaxRows = 65536;  // levels up to this size aggregate on one cluster
+
+template <class Bar>
+__device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
+    const Bar grid{};
     const Csr& A = g.A;
     const int n = A.n;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -529,7 +593,11 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
         }
         grid.sync();
         // admission fixpoint (uncapped sweeps of K/numba_backend.py:235-273)
-        volatile uint8_t* adm = g.adm;
+        // Plain (L1-cacheable) reads: a read may miss an admission made in
+        // the same sweep, which only defers it to the next sweep -- the
+        // fixpoint (and so the result) is the same; grid.sync() between
+        // sweeps makes every earlier admission visible.
+        uint8_t* adm = g.adm;
         while (true) {
             const int slot = itg % 3;
             if (tid == 0) ctl[6 + (itg + 1) % 3] = 0;
@@ -539,10 +607,19 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
                 const int c = g.owner[j];
                 const int e0 = A.rp[j], e1 = A.rp[j + 1];
                 if (c < 0 || c == j || adm[j] || e1 - e0 > kLongRow) continue;
-                for (int e = e0; e < e1; ++e) {
-                    const int nb = __ldg(A.ci + e);
-                    if (adm[nb] && g.owner[nb] == c) { adm[j] = 1; ch = 1; break; }
+                bool f = false;
+                for (int eb = e0; eb < e1 && !f; eb += 8) {
+                    int nb[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) nb[q] = eb + q < e1 ? __ldg(A.ci + eb + q) : j;  // j: not admitted
+                    uint8_t av[8];
+                    int ov[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) { av[q] = adm[nb[q]]; ov[q] = g.owner[nb[q]]; }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) f |= av[q] && ov[q] == c;
                 }
+                if (f) { adm[j] = 1; ch = 1; }
             }
             for (int t = w; t < nlong; t += nw) {
                 const int j = g.longs[t];
@@ -551,9 +628,16 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
                 const int e0 = A.rp[j], e1 = A.rp[j + 1];
                 if (c < 0 || c == j || adm[j]) continue;
                 bool f = false;
-                for (int e = e0 + lane; e < e1 && !f; e += 32) {
-                    const int nb = __ldg(A.ci + e);
-                    f = adm[nb] && g.owner[nb] == c;
+                for (int e = e0 + lane; e < e1 && !f; e += 128) {
+                    int nb[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) nb[q] = e + 32 * q < e1 ? __ldg(A.ci + e + 32 * q) : j;  // j: not admitted
+                    uint8_t av[4];
+                    int ov[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) { av[q] = adm[nb[q]]; ov[q] = g.owner[nb[q]]; }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) f |= av[q] && ov[q] == c;
                 }
                 if (__any_sync(0xffffffffu, f) && lane == 0) { adm[j] = 1; ch = 1; }
             }
@@ -593,6 +677,11 @@ __global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) {
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         g.prof[4 * min(pass, 32)] = t;
     }
+}
+
+__global__ void __launch_bounds__(256) k_aggregate_coop(AggCoop g) { k_aggregate_body<GridBar>(g); }
+__global__ void __launch_bounds__(kAggClusterThreads, 1) k_aggregate_cluster(AggCoop g) {
+    k_aggregate_body<ClusterBar>(g);
 }
 
 // ============================================================ renumbering
@@ -1056,9 +1145,33 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         }
         // one vertex per thread up to full residency: the passes are
         // latency-bound, fewer CTAs (cheaper barriers) measured slower
-        const int blocks = std::max(1, std::min(max_blocks, cdiv(n, 256)));
-        void* args[] = {&g};
-        UA_CK(cudaLaunchCooperativeKernel((void*)k_aggregate_coop, blocks, 256, args, 0, s));
+        int blocks = std::max(1, std::min(max_blocks, cdiv(n, 256)));
+        static const bool no_cluster = getenv("UAAMG_AGG_NO_CLUSTER") != nullptr;  // A/B diagnostics
+        if (n <= kAggClusterMaxRows && !no_cluster) {
+            // small level: every pass is a chain of latency-bound phases;
+            // one 16-CTA cluster with hardware barriers instead of the grid
+            static bool attr = false;
+            if (!attr) {
+                UA_CK(cudaFuncSetAttribute(k_aggregate_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                attr = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kAggClusterCtas);
+            cfg.blockDim = dim3(kAggClusterThreads);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kAggClusterCtas;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            UA_CK(cudaLaunchKernelEx(&cfg, k_aggregate_cluster, g));
+            blocks = kAggClusterCtas;
+        } else {
+            void* args[] = {&g};
+            UA_CK(cudaLaunchCooperativeKernel((void*)k_aggregate_coop, blocks, 256, args, 0, s));
+        }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         UA_CK(cudaMemcpyAsync(h_cnt, ctl.p + 9, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         UA_CK(cudaStreamSynchronize(s));
