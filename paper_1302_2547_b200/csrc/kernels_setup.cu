@@ -828,6 +828,106 @@ __global__ void k_galerkin_accum_int(Csr A, const int* __restrict__ v2a, const i
         for (int e = e0 + lane; e < e1; e += 32) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
     }
 }
+// Integer path on levels whose aggregate streams are all short (fine
+// levels), one warp per aggregate I: its coarse row accumulated in a
+// warp-private open-addressing table in shared memory, the member rows'
+// entries flattened across the lanes 32 at a time (a shuffle scan of the
+// member row lengths + a shuffle binary search per entry), then the nonzero
+// entries compacted, unsorted, into tk/tv at soff[I] and their count into
+// cnt[I].  Exact for integer values (any order), like the global tables of
+// k_galerkin_accum_int, without scattered DRAM atomics.
+constexpr int kGalWarps = 8;
+constexpr int kGalStreamMax = 256;          // levels whose longest stream is longer take the global tables
+constexpr int kGalCap = 2 * kGalStreamMax;  // shared-memory table slots per warp (load <= 1/2)
+__global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int nc, const int* __restrict__ v2a,
+                                                                     const int* __restrict__ agg_ptr,
+                                                                     const int* __restrict__ members,
+                                                                     const int* __restrict__ soff,
+                                                                     const int* __restrict__ slen, int* tk,
+                                                                     double* tv, int* cnt) {
+    __shared__ int sk[kGalWarps][kGalCap];
+    __shared__ double sv[kGalWarps][kGalCap];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int I = blockIdx.x * kGalWarps + wib; I < nc; I += gridDim.x * kGalWarps) {
+        const int L = slen[I];
+        const int need = 2 * min(L, nc);  // distinct coarse columns <= min(stream, nc)
+        int cap = 32;
+        while (cap < need) cap <<= 1;  // <= kGalCap on this path (every stream <= kGalStreamMax)
+        int* K = sk[wib];
+        double* V = sv[wib];
+        for (int t = lane; t < cap; t += 32) {
+            K[t] = -1;
+            V[t] = 0.0;
+        }
+        __syncwarp();
+        const int m0 = agg_ptr[I], m1 = agg_ptr[I + 1];
+        for (int mb = m0; mb < m1; mb += 32) {
+            const int m = mb + lane < m1 ? members[mb + lane] : -1;
+            const int rb = m >= 0 ? A.rp[m] : 0;
+            const int len = m >= 0 ? A.rp[m + 1] - rb : 0;
+            int pre = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, pre, 31);
+            const int excl = pre - len;
+            for (int base = 0; base < total; base += 32) {
+                const int sidx = base + lane;
+                int j = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int c = j + step;
+                    const int ex = __shfl_sync(0xffffffffu, excl, c & 31);
+                    if (c < 32 && ex <= sidx) j = c;
+                }
+                const int rbj = __shfl_sync(0xffffffffu, rb, j);
+                const int exj = __shfl_sync(0xffffffffu, excl, j);
+                if (sidx < total) {
+                    const int e = rbj + (sidx - exj);
+                    gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+                }
+            }
+        }
+        __syncwarp();
+        int c = 0;
+        const size_t o = (size_t)soff[I];
+        for (int t0 = 0; t0 < cap; t0 += 32) {
+            const int t = t0 + lane;
+            int key = -1;
+            double v = 0.0;
+            if (t < cap) {
+                key = K[t];
+                v = V[t];
+            }
+            const bool keep = key >= 0 && v != 0.0;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = c + __popc(bal & ((1u << lane) - 1u));
+                tk[o + pos] = key;
+                tv[o + pos] = v;
+            }
+            c += __popc(bal);
+        }
+        if (lane == 0) cnt[I] = c;
+        __syncwarp();
+    }
+}
+// move each row's compacted entries to its CSR position
+__global__ void k_galerkin_place(int nc, const int* __restrict__ soff, const int* __restrict__ cnt,
+                                 const int* __restrict__ rp_c, const int* __restrict__ tk,
+                                 const double* __restrict__ tv, int* col_c, double* val_c) {
+    const int lane = threadIdx.x & 31;
+    for (int I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < nc; I += (gridDim.x * blockDim.x) >> 5) {
+        const size_t o = (size_t)soff[I];
+        const int b = rp_c[I];
+        for (int t = lane; t < cnt[I]; t += 32) {
+            col_c[b + t] = tk[o + t];
+            val_c[b + t] = tv[o + t];
+        }
+    }
+}
 __global__ void k_galerkin_count(int nc, const int* __restrict__ soff, const int* __restrict__ slen,
                                  const int* __restrict__ hkey, const double* __restrict__ hval, int* cnt) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1274,12 +1374,39 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     const size_t hsz = 2 * (size_t)std::max(A.nnz, 1);
     SPtr<int> hkey{scratch<int>(0, hsz)};
     SPtr<double> hval{scratch<double>(1, hsz)};
-    UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
-    UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
-    if (integer_exact(A, s)) {
+    const bool exact_int = integer_exact(A, s);
+    SPtr<int> tk{nullptr};
+    SPtr<double> tv{nullptr};
+    // warp-per-aggregate shared-memory tables when every aggregate's stream
+    // is short (fine levels); otherwise (hub aggregates of coarse levels) the
+    // all-threads global table, whose parallelism does not depend on the
+    // longest stream
+    bool warp_path = false;
+    if (exact_int) {
+        DBuf<int> mx(1, s);
+        size_t tmp = 0;
+        UA_CK(cub::DeviceReduce::Max(nullptr, tmp, slen.p, mx.p, nc, s));
+        DBuf<char> t(tmp, s);
+        UA_CK(cub::DeviceReduce::Max(t.p, tmp, slen.p, mx.p, nc, s));
+        int h_mx = 0;
+        UA_CK(cudaMemcpyAsync(&h_mx, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        warp_path = h_mx <= kGalStreamMax;
+    }
+    if (exact_int && !warp_path) {
+        UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
+        UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
         UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, v2a, soff.p, slen.p, hkey.p, hval.p);
         UA_LAUNCH(k_galerkin_count, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, cnt.p);
+    } else if (exact_int) {
+        tk.p = scratch<int>(14, (size_t)std::max(A.nnz, 1));
+        tv.p = scratch<double>(15, (size_t)std::max(A.nnz, 1));
+        UA_LAUNCH(k_galerkin_int_warp, std::min(cdiv(nc, kGalWarps), 148 * 16), 32 * kGalWarps, 0, s, A, nc, v2a,
+                  agg_ptr, members, soff.p, slen.p, tk.p, tv.p, cnt.p);
+
     } else {
+        UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
+        UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
         UA_LAUNCH(k_galerkin_accum, cdiv(nc, 8), 256, 0, s, A, v2a, nc, agg_ptr, members, soff.p, slen.p, hkey.p,
                   hval.p, cnt.p);
     }
@@ -1294,8 +1421,12 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     if (nnz_c > 0) {
         DBuf<int> ck(nnz_c, s);
         DBuf<double> cv(nnz_c, s);
-        UA_LAUNCH(k_galerkin_compact, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ck.p,
-                  cv.p);
+        if (warp_path)
+            UA_LAUNCH(k_galerkin_place, std::min(cdiv(nc, 8), 148 * 16), 256, 0, s, nc, soff.p, cnt.p, rp_c.p, tk.p,
+                      tv.p, ck.p, cv.p);
+        else
+            UA_LAUNCH(k_galerkin_compact, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ck.p,
+                      cv.p);
         size_t tmp = 0;
         UA_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
                                                   rp_c.p + 1, s));

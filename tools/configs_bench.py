@@ -44,6 +44,9 @@ def build(name):
     elif name == "C4":
         A = problems.grid3d_device(256, 27)
         desc = "3D 27-point 256^3 (single GPU)"
+    elif name == "C5":
+        A = problems.grid3d_device(512, 7)
+        desc = "3D 7-point 512^3 (the full C5 problem on ONE GPU)"
     elif name == "C5x":
         A = problems.grid3d_device(None, 7, dims=(512, 512, 64))
         desc = "3D 7-point 512x512x64 (1/8 of C5: one GPU's slab)"
