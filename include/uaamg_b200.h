@@ -126,11 +126,14 @@ typedef struct {
     int n0;                 /* setup(n0=100)                                     */
     int max_levels;         /* setup(max_levels=20)                              */
     int singular;           /* -1 auto (detect_singular), 0/1 forced             */
+    int borrow;             /* 1: level 0 aliases the caller's arrays (they must
+                               outlive the hierarchy, as the reference's Level 0
+                               holds the caller's matrix); 0: copied          */
 } uaamg_setup_params;
 
 /* U/hierarchy.py:120-153.  Matrix arrays are device pointers, copied into
- * the hierarchy.  Returns UAAMG_ESETUP on stagnation (message as the
- * reference's SetupError). */
+ * the hierarchy unless params->borrow.  Returns UAAMG_ESETUP on stagnation
+ * (message as the reference's SetupError). */
 int uaamg_setup(int n, int64_t nnz, const int *row_ptr, const int *col, const double *val,
                 const uaamg_setup_params *params, uaamg_hierarchy **out, void *stream);
 void uaamg_hierarchy_free(uaamg_hierarchy *h);

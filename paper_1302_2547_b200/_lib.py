@@ -29,7 +29,7 @@ _d = ctypes.c_double
 
 class SetupParams(ctypes.Structure):
     _fields_ = [("size_cap", _i64), ("seed", _u64), ("max_passes", _i), ("passes_per_level", _i),
-                ("n0", _i), ("max_levels", _i), ("singular", _i)]
+                ("n0", _i), ("max_levels", _i), ("singular", _i), ("borrow", _i)]
 
 
 class HierarchyInfo(ctypes.Structure):

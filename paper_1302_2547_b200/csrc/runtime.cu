@@ -180,12 +180,19 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     auto L0 = std::make_unique<Level>();
     L0->n = n;
     L0->nnz = nnz;
-    L0->rp.alloc(n + 1, s);
-    L0->ci.alloc(std::max(nnz, 1ll), s);
-    L0->av.alloc(std::max(nnz, 1ll), s);
-    UA_CK(cudaMemcpyAsync(L0->rp.p, rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
-    UA_CK(cudaMemcpyAsync(L0->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
-    UA_CK(cudaMemcpyAsync(L0->av.p, av, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    if (P.borrow) {
+        // level 0 aliases the caller's arrays (U/hierarchy.py: Level 0 holds A)
+        L0->rp.adopt_view(const_cast<int*>(rp), n + 1);
+        L0->ci.adopt_view(const_cast<int*>(ci), std::max(nnz, 1ll));
+        L0->av.adopt_view(const_cast<double*>(av), std::max(nnz, 1ll));
+    } else {
+        L0->rp.alloc(n + 1, s);
+        L0->ci.alloc(std::max(nnz, 1ll), s);
+        L0->av.alloc(std::max(nnz, 1ll), s);
+        UA_CK(cudaMemcpyAsync(L0->rp.p, rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+        UA_CK(cudaMemcpyAsync(L0->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+        UA_CK(cudaMemcpyAsync(L0->av.p, av, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    }
     mark("copy");
     finish_level(*L0, s);
     mark("groups0");

@@ -101,8 +101,9 @@ class CoarseSolver:
 class Hierarchy:
     """Device-resident multilevel hierarchy (reference hierarchy.py:74-109)."""
 
-    def __init__(self, handle, offset=0, parent=None):
+    def __init__(self, handle, offset=0, parent=None, matrix_owner=None):
         self._handle = handle
+        self._matrix_owner = matrix_owner
         self._offset = offset
         self._parent = parent
         L = _lib.load()
@@ -182,8 +183,9 @@ def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0
     P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
                          max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
                          n0=int(n0), max_levels=int(max_levels),
-                         singular=-1 if singular is None else int(bool(singular)))
+                         singular=-1 if singular is None else int(bool(singular)), borrow=1)
     h = ctypes.c_void_p()
     _lib.check(_lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
                                        ctypes.byref(h), stream()))
-    return Hierarchy(h)
+    # level 0 aliases the device matrix (as the reference's Level 0 holds A)
+    return Hierarchy(h, matrix_owner=d)
