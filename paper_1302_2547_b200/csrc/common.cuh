@@ -148,6 +148,31 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Block-wide maximum of T (int / unsigned long long / double), valid in
+// thread 0 -- lets a kernel issue ONE atomicMax per block instead of one per
+// thread (same-address atomics serialise at the L2).  All threads call it.
+template <class T>
+__device__ __forceinline__ T block_max(T v) {
+    __shared__ T wm[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const T u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = u > v ? u : v;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : wm[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = u > v ? u : v;
+        }
+    }
+    return v;
+}
+
 // Deterministic block sum (fixed shuffle tree + fixed smem order).  All
 // threads of the block must call it; result valid in every thread.
 template <int NT>

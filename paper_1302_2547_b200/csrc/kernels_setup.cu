@@ -951,8 +951,9 @@ __global__ void k_int_check(long long m, const double* __restrict__ v, int* noni
         bad |= (a != rint(a));
         mx = fmax(mx, fabs(a));
     }
-    if (bad) atomicOr(nonint, 1);
-    atomicMax(maxabs, (unsigned long long)__double_as_longlong(mx));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonint, 1);
+    mx = block_max(mx);
+    if (threadIdx.x == 0) atomicMax(maxabs, (unsigned long long)__double_as_longlong(mx));
 }
 
 // Phase C: compact the nonzero (J, value) pairs of row I to its output slot

@@ -196,7 +196,8 @@ __global__ void k_tile_nnz_max(int n, const int* rp, int* out) {  // rp: first r
     int m = 0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
         m = max(m, rp[min((t + 1) * kTmaRows, n)] - rp[t * kTmaRows]);
-    atomicMax(out, m);
+    m = block_max(m);
+    if (threadIdx.x == 0) atomicMax(out, m);
 }
 
 int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base) {

@@ -36,7 +36,8 @@ thread_local std::string g_last_error;
 __global__ void k_maxabs_vals(int m, const double* v, unsigned long long* out) {
     double mx = 0.0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) mx = fmax(mx, fabs(v[i]));
-    atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+    mx = block_max(mx);  // max of non-negative doubles = max of their bit patterns
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
 }
 __global__ void k_fill(int n, double* v, double x) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = x;
