@@ -726,6 +726,9 @@ __global__ void k_stream_len(int nc, const int* agg_ptr, const int* members, con
 }
 
 __device__ __forceinline__ unsigned hslot(int key, int cap) { return ((unsigned)key * 2654435761u) % (unsigned)cap; }
+// table capacity of aggregate I's coarse row: at most min(stream length, nc)
+// distinct coarse columns, load factor <= 1/2 (fits the 2*slen region at 2*soff)
+__device__ __forceinline__ int gal_cap(int L, int nc) { return 2 * min(L, nc); }
 
 // Phase A: one warp per aggregate I accumulates its coarse row in an
 // open-addressing table at hkey/hval[2*soff[I] .. +2*slen[I]).  The stream
@@ -740,7 +743,7 @@ __global__ void k_galerkin_accum(Csr A, const int* __restrict__ v2a, int nc, con
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = blockIdx.x * 8 + wib;
     if (I >= nc) return;
-    const int cap = 2 * slen[I];
+    const int cap = gal_cap(slen[I], nc);
     int* K = hkey + 2 * (size_t)soff[I];
     double* V = hval + 2 * (size_t)soff[I];
     for (int q = agg_ptr[I]; q < agg_ptr[I + 1]; ++q) {
@@ -804,7 +807,7 @@ __device__ __forceinline__ void gal_insert_add(int* K, double* V, int cap, int J
     }
     atomicAdd(V + slot, a);
 }
-__global__ void k_galerkin_accum_int(Csr A, const int* __restrict__ v2a, const int* __restrict__ soff,
+__global__ void k_galerkin_accum_int(Csr A, int nc, const int* __restrict__ v2a, const int* __restrict__ soff,
                                      const int* __restrict__ slen, int* hkey, double* hval) {
     // short rows: one thread per row; rows longer than kLongRow: one warp per row
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
@@ -812,7 +815,7 @@ __global__ void k_galerkin_accum_int(Csr A, const int* __restrict__ v2a, const i
         const int e0 = A.rp[r], e1 = A.rp[r + 1];
         if (e1 - e0 > kLongRow) continue;
         const int I = v2a[r];
-        const int cap = 2 * slen[I];
+        const int cap = gal_cap(slen[I], nc);
         int* K = hkey + 2 * (size_t)soff[I];
         double* V = hval + 2 * (size_t)soff[I];
         for (int e = e0; e < e1; ++e) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
@@ -822,7 +825,7 @@ __global__ void k_galerkin_accum_int(Csr A, const int* __restrict__ v2a, const i
         const int e0 = A.rp[r], e1 = A.rp[r + 1];
         if (e1 - e0 <= kLongRow) continue;
         const int I = v2a[r];
-        const int cap = 2 * slen[I];
+        const int cap = gal_cap(slen[I], nc);
         int* K = hkey + 2 * (size_t)soff[I];
         double* V = hval + 2 * (size_t)soff[I];
         for (int e = e0 + lane; e < e1; e += 32) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
@@ -850,7 +853,7 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int I = blockIdx.x * kGalWarps + wib; I < nc; I += gridDim.x * kGalWarps) {
         const int L = slen[I];
-        const int need = 2 * min(L, nc);  // distinct coarse columns <= min(stream, nc)
+        const int need = gal_cap(L, nc);
         int cap = 32;
         while (cap < need) cap <<= 1;  // <= kGalCap on this path (every stream <= kGalStreamMax)
         int* K = sk[wib];
@@ -933,7 +936,7 @@ __global__ void k_galerkin_count(int nc, const int* __restrict__ soff, const int
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = blockIdx.x * 8 + wib;
     if (I >= nc) return;
-    const int cap = 2 * slen[I];
+    const int cap = gal_cap(slen[I], nc);
     const int* K = hkey + 2 * (size_t)soff[I];
     const double* V = hval + 2 * (size_t)soff[I];
     int c = 0;
@@ -964,7 +967,7 @@ __global__ void k_galerkin_compact(int nc, const int* __restrict__ soff, const i
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = blockIdx.x * 8 + wib;
     if (I >= nc) return;
-    const int cap = 2 * slen[I];
+    const int cap = gal_cap(slen[I], nc);
     const int* K = hkey + 2 * (size_t)soff[I];
     const double* V = hval + 2 * (size_t)soff[I];
     int base = rp_c[I];
@@ -1397,7 +1400,7 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     if (exact_int && !warp_path) {
         UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
         UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
-        UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, v2a, soff.p, slen.p, hkey.p, hval.p);
+        UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, nc, v2a, soff.p, slen.p, hkey.p, hval.p);
         UA_LAUNCH(k_galerkin_count, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, cnt.p);
     } else if (exact_int) {
         tk.p = scratch<int>(14, (size_t)std::max(A.nnz, 1));

@@ -7,7 +7,7 @@
 
 namespace uaamg {
 
-constexpr int kTailThreads = 512;
+constexpr int kTailThreads = 576;
 constexpr int kTailWarps = kTailThreads / 32;
 constexpr int kTailMaxCs = 16;
 constexpr int kTailLongMin = 256;  // same row split as the solve's group kernels (kSolveLongMin)
