@@ -488,7 +488,7 @@ struct ClusterBar {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 };
-constexpr int kAggClusterThreads = 512;
+constexpr int kAggClusterThreads = 1024;
 constexpr int kAggClusterCtas = 16;
 constexpr int kAggClusterMaxRows = 65536;  // levels up to this size aggregate on one cluster
 
