@@ -21,6 +21,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <chrono>
 #include <vector>
 
 #include "csr_tma.cuh"
@@ -170,12 +171,15 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     // UAAMG_SETUP_PROF=1: per-phase stream time (diagnostics)
     static const bool sprof = getenv("UAAMG_SETUP_PROF") != nullptr;
     std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    std::vector<double> host_t;  // host wall clock at each mark (enqueue side)
     auto mark = [&](const std::string& tag) {
         if (!sprof) return;
         cudaEvent_t e;
         UA_CK(cudaEventCreate(&e));
         UA_CK(cudaEventRecord(e, s));
         marks.push_back({tag, e});
+        host_t.push_back(std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now().time_since_epoch()).count());
     };
     mark("start");
     auto L0 = std::make_unique<Level>();
@@ -231,7 +235,17 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     for (size_t k = 1; k < marks.size(); ++k) {
         float t = 0;
         cudaEventElapsedTime(&t, marks[k - 1].second, marks[k].second);
-        fprintf(stderr, "setup %-16s %8.3f ms\n", marks[k].first.c_str(), t);
+        fprintf(stderr, "setup %-16s %8.3f ms  (host %8.3f ms)\n", marks[k].first.c_str(), t, host_t[k] - host_t[k - 1]);
+    }
+    if (sprof) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        cudaGetDevice(&dev);
+        cudaDeviceGetDefaultMemPool(&pool, dev);
+        uint64_t res = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        fprintf(stderr, "setup pool reserved %.1f MB used %.1f MB\n", res / 1e6, used / 1e6);
     }
     for (auto& m : marks) cudaEventDestroy(m.second);
     float ms = 0;

@@ -11,6 +11,7 @@ level matrices/aggregations are materialised lazily on attribute access.
 """
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -37,6 +38,33 @@ class _LazyMatrix:
     """Host SparseMatrix of a device level, materialised on first use."""
 
 
+class _Native:
+    """Owns the native hierarchy handle (and the device matrix level 0
+    aliases).  Levels and device views hold this object rather than the
+    Hierarchy, so there is no reference cycle and the device memory is
+    released as soon as the last user goes away, not at a later cyclic GC
+    pass (which would free many hierarchies at once, at an arbitrary point)."""
+
+    __slots__ = ("handle", "matrix_owner", "__weakref__")
+
+    def __init__(self, handle, matrix_owner=None):
+        self.handle = handle
+        self.matrix_owner = matrix_owner
+
+    def level_view(self, l):
+        v = _lib.LevelView()
+        _lib.check(_lib.load().uaamg_hierarchy_level(self.handle, l, ctypes.byref(v)))
+        return v
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            try:
+                _lib.load().uaamg_hierarchy_free(self.handle)
+            except Exception:
+                pass
+            self.handle = None
+
+
 class Level:
     """One hierarchy level: ``matrix`` (host SparseMatrix, lazy) and
     ``aggregation`` (None on the coarsest level); ``device_matrix`` is the
@@ -44,12 +72,12 @@ class Level:
 
     __slots__ = ("_h", "_l", "_matrix", "_agg", "_dev")
 
-    def __init__(self, h, l):
-        self._h, self._l = h, l
+    def __init__(self, native, l):
+        self._h, self._l = native, l  # the native owner (no back-reference to the Hierarchy)
         self._matrix = self._agg = self._dev = None
 
     def _view(self):
-        return self._h._level_view(self._l)
+        return self._h.level_view(self._l)
 
     @property
     def device_matrix(self):
@@ -89,13 +117,14 @@ class CoarseSolver:
     (Cholesky-based inverse, or eigen pseudo-inverse when singular)."""
 
     def __init__(self, h):
-        self._h = h
+        self._h = weakref.ref(h)  # no cycle through the Hierarchy
         self.n = h.levels[-1].n
         self.singular = h.singular
 
     def solve(self, b):
         from .solvers import CycleSpec, Smoother, cycle
-        return cycle(self._h, CycleSpec(), Smoother(), self._h.n_levels - 1, b)
+        h = self._h()
+        return cycle(h, CycleSpec(), Smoother(), h.n_levels - 1, b)
 
 
 class Hierarchy:
@@ -103,7 +132,7 @@ class Hierarchy:
 
     def __init__(self, handle, offset=0, parent=None, matrix_owner=None):
         self._handle = handle
-        self._matrix_owner = matrix_owner
+        self._native = parent._native if parent is not None else _Native(handle, matrix_owner)
         self._offset = offset
         self._parent = parent
         L = _lib.load()
@@ -112,7 +141,7 @@ class Hierarchy:
         self._info = info
         self.singular = bool(info.singular)
         nl = info.n_levels - offset
-        self.levels = [Level(self, offset + l) for l in range(nl)]
+        self.levels = [Level(self._native, offset + l) for l in range(nl)]
         n0 = self.levels[0].n
         nnz0 = max(self.levels[0].nnz, 1)
         self.grid_complexity = sum(l.n for l in self.levels) / n0
@@ -121,9 +150,7 @@ class Hierarchy:
         self.coarsest_solver = CoarseSolver(self)
 
     def _level_view(self, l):
-        v = _lib.LevelView()
-        _lib.check(_lib.load().uaamg_hierarchy_level(self._handle, l, ctypes.byref(v)))
-        return v
+        return self._native.level_view(l)
 
     @property
     def n_levels(self):
@@ -148,14 +175,6 @@ class Hierarchy:
             rows.append(row)
         return {"levels": rows, "grid_complexity": self.grid_complexity,
                 "operator_complexity": self.operator_complexity, "singular": self.singular}
-
-    def __del__(self):
-        if getattr(self, "_parent", None) is None and getattr(self, "_handle", None):
-            try:
-                _lib.load().uaamg_hierarchy_free(self._handle)
-            except Exception:
-                pass
-            self._handle = None
 
     def __repr__(self):
         return f"Hierarchy(levels={[l.n for l in self.levels]})"
