@@ -90,7 +90,12 @@ struct NpcgState {
     int max_iters;
     int err_level;
     double err_drift;
+    int* host_active;  // mapped pinned mirror of `active` (host polls it; nullptr: none)
 };
+// write the host mirror of NpcgState::active (system-scope store)
+__device__ __forceinline__ void npcg_mirror(NpcgState* st) {
+    if (st->host_active) *(volatile int*)st->host_active = st->active;
+}
 
 // Reduction scratch shared by all reductions on one stream (sequential use).
 struct RedScratch {

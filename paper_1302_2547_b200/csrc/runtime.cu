@@ -74,7 +74,8 @@ static bool detect_singular(const Level& L, cudaStream_t s) {
 static void finish_level(Level& L, cudaStream_t s) {
     build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s);
     static const bool no_tma = getenv("UAAMG_NO_TMA") != nullptr;  // A/B diagnostics
-    if (!no_tma && L.n >= kTmaMinRows && L.grp.g.np == 0) {
+    static const long long tma_min = getenv("UAAMG_TMA_MIN_ROWS") ? atoll(getenv("UAAMG_TMA_MIN_ROWS")) : kTmaMinRows;
+    if (!no_tma && L.n >= tma_min && L.grp.g.np == 0) {
         const int cap = max_tile_nnz(L.n, L.rp.p, s);
         if (cap <= kTmaMaxCap) L.grp.g.tma_cap = std::max(cap, 4);
     }
@@ -314,7 +315,8 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
     ws->r.alloc(n0, s); ws->z.alloc(n0, s); ws->p0.alloc(n0, s); ws->p1.alloc(n0, s);
     ws->ap0.alloc(n0, s); ws->ap1.alloc(n0, s); ws->bproj.alloc(n0, s);
     ws->hist.alloc((size_t)p.max_iters + 1, s);
-    UA_CK(cudaMallocHost(&ws->h_flags, 4 * sizeof(int)));
+    UA_CK(cudaHostAlloc(&ws->h_flags, 4 * sizeof(int), cudaHostAllocMapped));
+    UA_CK(cudaHostGetDevicePointer((void**)&ws->d_flags, ws->h_flags, 0));
     UA_CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     UA_CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
@@ -429,9 +431,10 @@ static void build_graphs(Plan& pl, double* x) {
     ws->graphs_built = true;
 }
 
-__global__ void k_set_npcg(NpcgState* st, double tol, int max_iters) {
+__global__ void k_set_npcg(NpcgState* st, double tol, int max_iters, int* host_active) {
     st->tol = tol;
     st->max_iters = max_iters;
+    st->host_active = host_active;
 }
 
 static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const double* b, const double* x0, double* x,
@@ -475,7 +478,10 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
         UA_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
         launch_copy(n, bb, ws->r.p, s);
     }
-    UA_LAUNCH(k_set_npcg, 1, 1, 0, s, ws->npcg.p, p.tol, p.max_iters);
+    // the iteration loop polls a mapped pinned mirror of `active` written by
+    // the deciding kernels (no device-to-host copy between iteration graphs)
+    *(volatile int*)ws->h_flags = 1;
+    UA_LAUNCH(k_set_npcg, 1, 1, 0, s, ws->npcg.p, p.tol, p.max_iters, ws->d_flags);
     launch_npcg_init(n, bb, ws->r.p, ws->npcg.p, ws->hist.p, pl.rs(), s);
     UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
     // iterations: pipelined launches, at most one no-op iteration past the end
@@ -519,14 +525,17 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
             }
             ++launched;
             last_par = par;
-            UA_CK(cudaMemcpyAsync(ws->h_flags + par, &ws->npcg.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
+            static const bool flag_copy = getenv("UAAMG_FLAG_COPY") != nullptr;  // A/B diagnostics
+            if (flag_copy)
+                UA_CK(cudaMemcpyAsync(ws->h_flags, &ws->npcg.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
             UA_CK(cudaEventRecord(ws->ev[par], s));
             if (it >= 1) {
                 UA_CK(cudaEventSynchronize(ws->ev[par ^ 1]));
                 if (prof && before[par ^ 1]) harvest(par ^ 1);
-                before[par] = ws->h_flags[par ^ 1];
+                const int act = *(volatile int*)ws->h_flags;  // >= iteration it-1's decision
+                before[par] = act;
                 before[par ^ 1] = 0;
-                if (ws->h_flags[par ^ 1] == 0) { last_par = -1; break; }
+                if (act == 0) { last_par = -1; break; }
             }
         }
         if (last_par >= 0) {

@@ -81,7 +81,8 @@ struct SolveWs {
     int64_t prof_count = 0;
     bool graphs_built = false;
     double* graph_x = nullptr;  // graphs bake in the iterate pointer
-    int* h_flags = nullptr;  // pinned
+    int* h_flags = nullptr;  // pinned, mapped: [0] mirror of NpcgState::active
+    int* d_flags = nullptr;  // its device address
     cudaEvent_t ev[2] = {nullptr, nullptr};
     ~SolveWs() {
         for (auto& g : graph) if (g) cudaGraphExecDestroy(g);

@@ -427,6 +427,7 @@ void Sharded::npcg_iteration(int parity) {
 }
 
 __global__ void k_set_npcg_sh(NpcgState* st, double tol, int max_iters) {
+    st->host_active = nullptr;
     st->tol = tol;
     st->max_iters = max_iters;
 }

@@ -315,6 +315,7 @@ struct EpiDirNpcg {
             st->status = 1;
             st->active = 0;
             st->alpha = 0.0;
+            npcg_mirror(st);
         } else {
             st->alpha = t[1] / t[0];
         }
@@ -562,6 +563,7 @@ struct BodyNpcgUpd : BodyBase {
         if (st->up >= 2) { st->have_prev = 0; st->up = 0; }
         else st->have_prev = 1;
         if (!(rel > st->tol) || st->iters >= st->max_iters) st->active = 0;
+        npcg_mirror(st);
     }
 };
 
@@ -606,6 +608,7 @@ struct BodyNpcgProj : BodyBase {
         if (st->up >= 2) { st->have_prev = 0; st->up = 0; }
         else st->have_prev = 1;
         if (!(rel > st->tol) || st->iters >= st->max_iters) st->active = 0;
+        npcg_mirror(st);
     }
 };
 
@@ -691,12 +694,14 @@ struct BodyNpcgInit : BodyBase {
             hist[0] = 0.0;
             st->last_rel = 0.0;
             st->active = 0;
+            npcg_mirror(st);
             return;
         }
         const double rel = sqrt(t[1]) / bn;
         hist[0] = rel;
         st->last_rel = rel;
         st->active = (rel > st->tol && st->max_iters > 0) ? 1 : 0;
+        npcg_mirror(st);
     }
 };
 
