@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "csr_tma.cuh"
 #include "tail.h"
 
 namespace uaamg {
@@ -540,12 +541,22 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant_
     const unsigned rank = cta_rank();
     if (a.prof && threadIdx.x < kTailProfMarks) g_tp[threadIdx.x] = threadIdx.x == 0 ? clock64() : 0;
     {
-        // static per-CTA data, before the dependency wait
-        const int4* src = reinterpret_cast<const int4*>(a.blob + (size_t)rank * a.L.blob_bytes);
-        int4* dst = reinterpret_cast<int4*>(sm);
-        for (int k = threadIdx.x; k < a.L.blob_bytes / 16; k += kTailThreads) dst[k] = __ldg(src + k);
+        // static per-CTA data, before the dependency wait: bulk copies
+        // (cp.async.bulk, mbarrier completion) instead of a load/store loop
+        __shared__ __align__(8) uint64_t stage_bar;
+        const unsigned char* src = a.blob + (size_t)rank * a.L.blob_bytes;
+        if (threadIdx.x == 0) {
+            mbar_init(&stage_bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&stage_bar, (unsigned)a.L.blob_bytes);
+            constexpr int kChunk = 32768;
+            for (int off = 0; off < a.L.blob_bytes; off += kChunk)
+                bulk_g2s(sm + off, src + off, (unsigned)min(kChunk, a.L.blob_bytes - off), &stage_bar);
+        }
+        __syncthreads();
+        mbar_wait(&stage_bar, 0);
     }
-    __syncthreads();
     pdl_wait();
     pdl_trigger();
     if (a.gate && *(volatile const int*)a.gate == 0) {  // same value in every CTA
