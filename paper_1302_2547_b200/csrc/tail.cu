@@ -445,7 +445,10 @@ __device__ void cred(TCtx& c, const double (&v)[K], double (&t)[K]) {
 // cycle(l) at the tail level from rin into z (U/solvers.py:128-157); the
 // coarse correction is the exact coarsest solve.  vapp >= 0: also form the
 // flexible-CG beta of the step that consumes z (fused beta dot); returns it.
-__device__ double tail_cycle(TCtx& c, int vin, int vz, int vapp, int vpp, double pap_prev, int m0) {
+// extra: a value to reduce along with the residual sum (single-aggregate
+// coarsest only; -1 disables): its cluster total is returned in *extra_out
+__device__ double tail_cycle(TCtx& c, int vin, int vz, int vapp, int vpp, double pap_prev, int m0,
+                             double extra = 0.0, double* extra_out = nullptr) {
     const TailArgs& a = *c.a;
     const TailHdr& hd = *c.hd;
     const int R = hd.R;
@@ -469,8 +472,13 @@ __device__ double tail_cycle(TCtx& c, int vin, int vz, int vapp, int vpp, double
         } else {
             for (int i = threadIdx.x; i < R; i += kTailThreads) s += rin[i];
         }
-        double t[1];
-        cred<1>(c, {s}, t);
+        double t[2];
+        if (extra_out) {
+            cred<2>(c, {s, extra}, t);
+            *extra_out = t[1];
+        } else {
+            cred<1>(c, {s}, *reinterpret_cast<double(*)[1]>(t));
+        }
         TP(m0 + 1);
         ec1 = __dmul_rn(a.minv0, t[0]);
     } else {
@@ -578,18 +586,33 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant_
         for (int i = threadIdx.x; i < R; i += kTailThreads) a.out[hd.row0 + i] = z[i];
         return;  // last cluster access was before tail_cycle's final barrier
     }
-    double tb[1];
-    cred<1>(c, {eb.s}, tb);
+    // ||b||: with a single-aggregate coarsest level it rides in the first
+    // cycle's residual reduction (a zero b then yields p'Ap = 0 below, the
+    // same "no update" outcome as the skipped FCG); otherwise its own
+    const bool fold_bn = a.nc == 1;
+    double bn2 = 0.0;
+    if (fold_bn) {
+        csync();  // b visible to the first cycle's gathers
+    } else {
+        double tb[1];
+        cred<1>(c, {eb.s}, tb);
+        bn2 = tb[0];
+    }
     TP(3);
-    const double bnorm = sqrt(tb[0]);
     int upd0 = 0;
-    if (!(bnorm <= 1e-14 * bnorm)) {  // EpiRestrictBegin::fin gate[0]
+    double bnorm = sqrt(bn2);
+    if (fold_bn || !(bnorm <= 1e-14 * bnorm)) {  // EpiRestrictBegin::fin gate[0]
         double pap_prev = 0.0;
         for (int k = 0; k < a.steps; ++k) {
             const int vin = k == 0 ? VB : VRF;
             const int pc = (k & 1) ? VP1 : VP0, pp = (k & 1) ? VP0 : VP1;
             const int apc = (k & 1) ? VAP1 : VAP0, app = (k & 1) ? VAP0 : VAP1;
-            const double beta = tail_cycle(c, vin, VZ, k > 0 ? app : -1, pp, pap_prev, 10 + 20 * k);
+            const double beta = tail_cycle(c, vin, VZ, k > 0 ? app : -1, pp, pap_prev, 10 + 20 * k, eb.s,
+                                           (fold_bn && k == 0) ? &bn2 : nullptr);
+            if (fold_bn && k == 0) {
+                bnorm = sqrt(bn2);
+                if (bnorm <= 1e-14 * bnorm) break;  // gate[0] = 0: b == 0, no update
+            }
             // direction p = z + beta pprev, Ap, p.Ap, p.r (EpiDirFcg)
             c.refresh(VZ, k > 0 ? pp : -1);
             EDir e{c.vec(vin), c.vec(pc), c.vec(apc), GDir{c.ref(VZ), c.ref(pp), k > 0, beta}, 0.0, 0.0};
@@ -608,6 +631,15 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant_
             const double* ap = c.vec(apc);
             const double* ri = c.vec(vin);
             double* rf = c.vec(VRF);
+            if (k == a.steps - 1) {
+                // last step: the residual and its norm (gate[steps]) have no
+                // reader -- only x leaves the tail
+                for (int i = threadIdx.x; i < R; i += kTailThreads) {
+                    const double xo = k == 0 ? 0.0 : x[i];
+                    x[i] = __dadd_rn(xo, __dmul_rn(alpha, p[i]));
+                }
+                break;
+            }
             double s = 0.0;
             for (int i = threadIdx.x; i < R; i += kTailThreads) {
                 const double xo = k == 0 ? 0.0 : x[i];
