@@ -5,6 +5,7 @@
 // Reference semantics: U/solvers.py (smoother_inverse_diag :69-81, smooth
 // :84-91, transfers :94-109, projections :112-125, cycle :128-157,
 // _inner_fcg :160-187, npcg_solve :190-255) and K/numba_backend.py kernels.
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -127,7 +128,8 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
 void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
                            RedScratch rs, double* part, unsigned* bar, Exec ex) {
-    if (ex.rec || G.tma_cap > 0) {
+    static const bool no_fuse = getenv("UAAMG_NO_DIR_FUSE") != nullptr;  // A/B diagnostics
+    if (ex.rec || G.tma_cap > 0 || no_fuse) {
         launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
         launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex);
         return;
