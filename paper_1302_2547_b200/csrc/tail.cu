@@ -203,15 +203,6 @@ struct EDir {  // p, Ap, p.Ap, p.r (EpiDirFcg)
     }
 };
 
-struct ESplit {  // a segment partial into its owner's split slot
-    const int* dst;
-    double* part;  // local address of the split partial array (same offset in every CTA)
-    __device__ void row(int i, double acc) {
-        const int d = dst[i];
-        *static_cast<double*>(__cluster_map_shared_rank(part + (d & 0xffff), (unsigned)d >> 16)) = acc;
-    }
-};
-
 struct RowSet {
     const int* rp;
     const int* idx;
@@ -373,30 +364,15 @@ struct TCtx {
     __device__ double* win() const { return reinterpret_cast<double*>(sm + a->L.win); }
     __device__ double* psum() const { return reinterpret_cast<double*>(sm + a->L.psum); }
     __device__ RowSet A() const { return rowset(sm, a->L.A, hd->R, hd->np, hd->nl); }
-    // A row sums incl. the split rows: segments everywhere, a cluster
-    // barrier, then each owner folds its split rows' partials in CTA order
     __device__ void mark(int k) const {
         if (a->prof) smark(k);
     }
+    // the tail level's row sums (optional diagnostics marks)
     template <class G, class E>
     __device__ void rowsA(const G& g, E& e, int mk = -1) const {
         mark(mk);
         rowsum<false>(A(), win(), psum(), g, e, self(), mk >= 0 ? mk + 10 : -1);
         mark(mk >= 0 ? mk + 1 : -1);
-        if (!a->split) return;
-        ESplit es{reinterpret_cast<const int*>(sm + a->L.segdst), reinterpret_cast<double*>(sm + a->L.splpart)};
-        rowsum<false>(rowset(sm, a->L.Seg, hd->nseg, hd->snp, hd->snl), win(), psum(), g, es, self());
-        mark(mk >= 0 ? mk + 2 : -1);
-        csync();
-        mark(mk >= 0 ? mk + 3 : -1);
-        const int lane = threadIdx.x & 31;
-        const double* part = reinterpret_cast<const double*>(sm + a->L.splpart);
-        const int* lr = reinterpret_cast<const int*>(sm + a->L.splrow);
-        for (int q = threadIdx.x >> 5; q < hd->nsplit; q += kTailWarps) {
-            double acc = lane < a->cs ? part[q * kTailMaxCs + lane] : 0.0;
-            acc = warp_sum(acc);
-            if (lane == 0) e.row(lr[q], acc);
-        }
     }
     // padding column for gathers: hub slot 0 (a local copy; no cluster traffic)
     __device__ int self() const { return (int)(kHub << 16); }
@@ -671,12 +647,8 @@ struct HostRows {
     std::vector<int4> pc;
 };
 
-// rows [r0, r1) of a CSR (global row pointer grp): local offsets, entries
-// mapped by f, long rows split into 256-entry pieces (build_groups' split)
-// long rows of a local CSR become 256-entry pieces (build_groups' split),
-// except rows `nopiece` marks (split rows, folded elsewhere)
-template <class P>
-void add_pieces(HostRows& h, P nopiece) {
+// long rows of a local CSR become 256-entry pieces (build_groups' split)
+inline void add_pieces(HostRows& h) {
     h.lptr.assign(1, 0);
     h.lrow.clear();
     h.pc.clear();
@@ -684,7 +656,7 @@ void add_pieces(HostRows& h, P nopiece) {
     const int R = (int)h.rp.size() - 1;
     for (int i = 0; i < R; ++i) {
         const int b = h.rp[i], e = h.rp[i + 1];
-        if (nopiece(i) || e - b <= kTailLongMin) continue;
+        if (e - b <= kTailLongMin) continue;
         for (int eb = b; eb < e; eb += kTailLongMin) h.pc.push_back(make_int4(i, eb, std::min(eb + kTailLongMin, e), slot++));
         h.lrow.push_back(i);
         h.lptr.push_back(slot);
@@ -693,8 +665,8 @@ void add_pieces(HostRows& h, P nopiece) {
 
 // rows [r0, r1) of a CSR (global row pointer grp): local offsets, entries
 // mapped by f
-template <class F, class P>
-HostRows slice_rows(int r0, int r1, const int* grp, const int* gidx, const double* gval, F f, P nopiece) {
+template <class F>
+HostRows slice_rows(int r0, int r1, const int* grp, const int* gidx, const double* gval, F f) {
     HostRows h;
     const int R = r1 - r0;
     h.rp.resize(R + 1);
@@ -707,12 +679,8 @@ HostRows slice_rows(int r0, int r1, const int* grp, const int* gidx, const doubl
         h.idx[k] = f(gidx[base + k]);
         if (gval) h.val[k] = gval[base + k];
     }
-    add_pieces(h, [&](int i) { return nopiece(r0 + i); });
+    add_pieces(h);
     return h;
-}
-template <class F>
-HostRows slice_rows(int r0, int r1, const int* grp, const int* gidx, const double* gval, F f) {
-    return slice_rows(r0, r1, grp, gidx, gval, f, [](int) { return false; });
 }
 
 struct Bump {
@@ -737,10 +705,9 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     // contiguous row blocks of about equal work: a warp unit is a 32-row
     // group or a 256-entry piece of a long row, so rows cost 1/32 unit and a
     // long row its piece count (a hub row gets a CTA of its own)
-    auto is_split = [&](int i) { return in.rp[i + 1] - in.rp[i] > kTailSplitMin; };
     auto cost = [&](int i) {
         const int len = in.rp[i + 1] - in.rp[i];
-        return len > kTailLongMin && !is_split(i) ? (double)((len + kTailLongMin - 1) / kTailLongMin) : 1.0 / 32;
+        return len > kTailLongMin ? (double)((len + kTailLongMin - 1) / kTailLongMin) : 1.0 / 32;
     };
     double total = 0;
     for (int i = 0; i < n; ++i) total += cost(i);
@@ -781,38 +748,14 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     auto pkA = [&](int k) { return hslot[k] >= 0 ? (int)((kHub << 16) | (unsigned)hslot[k]) : pk(k); };
     struct Cta {
         TailHdr h;
-        HostRows A, Min, Mout, Seg;
-        std::vector<int> segdst, splrow;
+        HostRows A, Min, Mout;
     };
     std::vector<Cta> ct(cs);
     size_t eA = 0, pA = 0, lA = 0, eM = 0, pM = 0, lM = 0, eC = 0, pC = 0, lC = 0;
-    size_t eS = 0, pS = 0, lS = 0, nS = 0, nSp = 0;
-    // split rows: owner slot q, and one segment per (split row, CTA)
-    std::vector<int> splits, qslot(n, -1);
-    for (int i = 0; i < n; ++i)
-        if (is_split(i)) {
-            qslot[i] = (int)ct[own[i]].splrow.size();
-            ct[own[i]].splrow.push_back(loc[i]);
-            splits.push_back(i);
-        }
-    for (int c = 0; c < cs; ++c) {
-        HostRows& g = ct[c].Seg;
-        g.rp.assign(1, 0);
-        for (int hrow : splits) {
-            for (int k = in.rp[hrow]; k < in.rp[hrow + 1]; ++k)
-                if (own[in.ci[k]] == c) {
-                    g.idx.push_back(pkA(in.ci[k]));
-                    g.val.push_back(in.av[k]);
-                }
-            g.rp.push_back((int)g.idx.size());
-            ct[c].segdst.push_back((own[hrow] << 16) | (qslot[hrow] * kTailMaxCs + c));
-        }
-        add_pieces(g, [](int) { return false; });
-    }
     for (int c = 0; c < cs; ++c) {
         const int r0 = cut[c], r1 = cut[c + 1];
         Cta& t = ct[c];
-        t.A = slice_rows(r0, r1, in.rp.data(), in.ci.data(), in.av.data(), pkA, is_split);
+        t.A = slice_rows(r0, r1, in.rp.data(), in.ci.data(), in.av.data(), pkA);
         t.Min = slice_rows(r0, r1, in.mp.data(), in.mem.data(), nullptr, [](int k) { return k; });
         std::memset(&t.h, 0, sizeof(t.h));
         t.h.R = r1 - r0;
@@ -832,14 +775,7 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
         eA = std::max(eA, t.A.idx.size()); pA = std::max(pA, t.A.pc.size()); lA = std::max(lA, t.A.lrow.size());
         eM = std::max(eM, t.Min.idx.size()); pM = std::max(pM, t.Min.pc.size()); lM = std::max(lM, t.Min.lrow.size());
         eC = std::max(eC, t.Mout.idx.size()); pC = std::max(pC, t.Mout.pc.size()); lC = std::max(lC, t.Mout.lrow.size());
-        t.h.nseg = (int)splits.size();
-        t.h.snp = (int)t.Seg.pc.size();
-        t.h.snl = (int)t.Seg.lrow.size();
-        t.h.nsplit = (int)t.splrow.size();
-        eS = std::max(eS, t.Seg.idx.size()); pS = std::max(pS, t.Seg.pc.size()); lS = std::max(lS, t.Seg.lrow.size());
-        nSp = std::max(nSp, t.splrow.size());
     }
-    nS = splits.size();
     // layout
     TailLayout L;
     Bump b;
@@ -855,11 +791,6 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     rows_layout(L.A, R, eA, pA, lA, true);
     rows_layout(L.Min, R, eM, pM, lM, false);
     if (dense) rows_layout(L.Mout, Rc, eC, pC, lC, false);
-    if (nS) {
-        rows_layout(L.Seg, (int)nS, eS, pS, lS, true);
-        L.segdst = b.take(sizeof(int) * nS);
-        L.splrow = b.take(sizeof(int) * std::max<size_t>(nSp, 1));
-    }
     L.invm = b.take(sizeof(double) * R);
     L.v2a = b.take(sizeof(int) * R);
     L.hinvm = b.take(sizeof(double) * kTailMaxHubs);
@@ -870,8 +801,7 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     L.rcmax = Rc;
     L.vec = b.take(sizeof(double) * (size_t)kTailVecs * R);
     L.win = b.take(sizeof(double) * kTailWarps * 256);
-    L.psum = b.take(sizeof(double) * std::max<size_t>({pA, pM, pC, pS, (size_t)1}));
-    if (nS) L.splpart = b.take(sizeof(double) * std::max<size_t>(nSp, 1) * kTailMaxCs);
+    L.psum = b.take(sizeof(double) * std::max<size_t>({pA, pM, pC, (size_t)1}));
     L.red = b.take(sizeof(double) * 2 * kTailMaxCs * 4);
     L.bsum = b.take(sizeof(double) * (kTailThreads / 32 + 1));
     L.cvec = b.take(sizeof(double) * (2 * std::max(Rc, 1) + std::max(in.nc, 1)));
@@ -898,11 +828,6 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
         put_rows(L.A, t.A, R);
         put_rows(L.Min, t.Min, R);
         if (dense) put_rows(L.Mout, t.Mout, Rc);
-        if (nS) {
-            put_rows(L.Seg, t.Seg, (int)nS);
-            std::memcpy(B + L.segdst, t.segdst.data(), sizeof(int) * t.segdst.size());
-            if (!t.splrow.empty()) std::memcpy(B + L.splrow, t.splrow.data(), sizeof(int) * t.splrow.size());
-        }
         const int r0 = t.h.row0;
         std::memcpy(B + L.invm, in.invm.data() + r0, sizeof(double) * t.h.R);
         for (int h = 0; h < (int)hubs.size(); ++h) {
@@ -948,7 +873,6 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     a.cs = cs;
     a.Rc = Rc;
     a.nhub = (int)hubs.size();
-    a.split = nS > 0 ? 1 : 0;
     for (int h = 0; h < a.nhub; ++h) a.hubpk[h] = pk(hubs[h]);
     a.nc = in.nc;
     a.pre = in.pre;

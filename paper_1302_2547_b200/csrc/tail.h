@@ -17,10 +17,6 @@ constexpr int kTailSmemMax = 226 * 1024;  // dynamic; leaves room for static sha
 // owning CTA's shared memory
 constexpr int kTailMaxHubs = 32;
 constexpr int kTailHubDeg = 128;
-// rows longer than this are split by column owner: every CTA sums the
-// entries whose columns it owns (local gathers) and the owner folds the
-// per-CTA partials in CTA order
-constexpr int kTailSplitMin = 1 << 30;  // (off: a hub row's pieces run on its own CTA)
 
 // A set of row sums owned by one CTA: rows [0, R) with entries
 // [rp[i], rp[i + 1]) of idx (and val unless unit).  Rows longer than
@@ -37,10 +33,6 @@ struct TailLayout {
     TailRows A;        // the tail level's matrix rows (idx: packed owner<<16 | local)
     TailRows Min;      // restriction into the tail level (idx: rows of the level above, global)
     TailRows Mout;     // restriction to a dense coarsest level (idx: packed)
-    TailRows Seg;      // this CTA's segments of the split rows (idx: packed, local columns)
-    int segdst = -1;   // ints per segment: packed (owner << 16 | split slot) of its partial
-    int splrow = -1;   // ints per owned split row: local row
-    int splpart = -1;  // doubles: owned split rows x kTailMaxCs partials
     int invm = -1;     // doubles, Rmax
     int v2a = -1;      // ints, Rmax (coarse index; dense coarsest only)
     int hinvm = -1;    // hub columns' smoother diagonal (doubles, kTailMaxHubs)
@@ -64,8 +56,7 @@ struct TailHdr {
     int mnp, mnl;      // restriction-in pieces / long rows
     int Rc, cnp, cnl;  // dense coarsest: owned coarse rows, pieces, long rows
     int row0, crow0;   // first owned row / coarse row
-    int nseg, snp, snl;  // split-row segments of this CTA, their pieces / long segments
-    int nsplit;          // owned split rows
+    int pad[4];
 };
 
 struct TailArgs {
@@ -74,7 +65,6 @@ struct TailArgs {
     int cs = 0;        // CTAs in the cluster
     int Rc = 0;        // coarse rows per CTA (dense coarsest; owner of coarse row j: j / Rc)
     int nhub = 0;
-    int split = 0;     // any split rows (cluster-uniform)
     int hubpk[kTailMaxHubs] = {};  // packed location (owner << 16 | local) of each hub column
     int nc = 0;        // coarsest size
     int pre = 1, post = 1;
