@@ -145,7 +145,9 @@ void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const doubl
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);
 
 // ---- elementwise / reductions ----
-void launch_inv_diag(const Csr& A, int l1, double omega, double* invm, int* bad_row, cudaStream_t s);
+// smoother diagonal: G = the level's solve groups (its long rows take a block each)
+void launch_inv_diag(const Csr& A, const GroupBuf& G, int l1, double omega, double* invm, int* bad_row,
+                     cudaStream_t s);
 void launch_xpre1(int n, const double* invm, const double* b, double* x, const int* gate, Exec ex);
 void launch_prolongate(int n, int xmode, const double* invm, const double* b, const double* xpre, const int* v2a,
                        const double* ec, const int* ec_valid, double* out, const int* gate, Exec ex);

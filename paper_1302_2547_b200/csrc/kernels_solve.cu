@@ -260,27 +260,70 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
 }
 
 // ---- smoother diagonal (U/solvers.py:69-81, K/numba_backend.py:59-84)
+// Rows of at most kSolveLongMin entries: a thread each, |a_ij| summed in
+// ascending order (K/numba_backend.py:71-84) with the loads batched 8 at a
+// time.  Longer rows (the solve path's piece rows) are skipped here and
+// done by k_inv_diag_long, a block per row (fixed block-tree order, like the
+// solve's long-row pieces).
+__device__ __forceinline__ void inv_diag_fin(int i, double acc, double dii, int l1, double omega, double* invm,
+                                             int* bad_row) {
+    const double m = l1 ? __dadd_rn(acc, dii) : dii;
+    if (m <= 0.0) atomicMin(bad_row, i);
+    invm[i] = (l1 ? 1.0 : omega) / m;
+}
 __global__ void k_inv_diag(Csr A, int l1, double omega, double* invm, int* bad_row) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        const int e0 = A.rp[i], e1 = A.rp[i + 1];
+        if (e1 - e0 > kSolveLongMin) continue;
         double acc = 0.0, dii = 0.0;
-        for (int k = A.rp[i]; k < A.rp[i + 1]; ++k) {
-            const int c = A.ci[k];
-            if (l1) {
-                if (c == i) dii = A.av[k];
-                else acc = __dadd_rn(acc, fabs(A.av[k]));
-            } else if (c == i) {
-                dii = A.av[k];
-                break;
+        bool seen = false;
+        for (int k0 = e0; k0 < e1; k0 += 8) {
+            int c[8];
+            double a[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = k0 + q < e1 ? A.ci[k0 + q] : -1;
+                a[q] = k0 + q < e1 ? A.av[k0 + q] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (c[q] < 0) continue;
+                if (l1) {
+                    if (c[q] == i) dii = a[q];  // l1: the last diagonal entry (loop over k)
+                    else acc = __dadd_rn(acc, fabs(a[q]));
+                } else if (c[q] == i && !seen) {
+                    dii = a[q];  // jacobi: the first diagonal entry (the loop breaks there)
+                    seen = true;
+                }
             }
         }
-        const double m = l1 ? __dadd_rn(acc, dii) : dii;
-        if (m <= 0.0) atomicMin(bad_row, i);
-        invm[i] = (l1 ? 1.0 : omega) / m;
+        inv_diag_fin(i, acc, dii, l1, omega, invm, bad_row);
     }
 }
+__global__ void k_inv_diag_long(Csr A, const int4* piece, const int* pbase, int l1, double omega, double* invm,
+                                int* bad_row) {
+    __shared__ double sm[kThreads / 32 + 1];
+    __shared__ double sd[kThreads / 32 + 1];
+    const int row = piece[pbase[blockIdx.x]].x;
+    const int e0 = A.rp[row], e1 = A.rp[row + 1];
+    double acc = 0.0, dii = 0.0;
+    for (int k = e0 + threadIdx.x; k < e1; k += blockDim.x) {
+        const int c = A.ci[k];
+        const double a = A.av[k];
+        if (c == row) dii = a;
+        else if (l1) acc = __dadd_rn(acc, fabs(a));
+    }
+    acc = block_sum<kThreads>(acc, sm);
+    dii = block_sum<kThreads>(dii, sd);  // the one diagonal entry (zeros elsewhere)
+    if (threadIdx.x == 0) inv_diag_fin(row, acc, dii, l1, omega, invm, bad_row);
+}
 
-void launch_inv_diag(const Csr& A, int l1, double omega, double* invm, int* bad_row, cudaStream_t s) {
+void launch_inv_diag(const Csr& A, const GroupBuf& G, int l1, double omega, double* invm, int* bad_row,
+                     cudaStream_t s) {
     UA_LAUNCH(k_inv_diag, map_grid(A.n) * 2, kThreads, 0, s, A, l1, omega, invm, bad_row);
+    const int nlong = G.pbase.n > 0 ? (int)G.pbase.n - 1 : 0;
+    if (nlong > 0 && G.g.long_min == kSolveLongMin)
+        UA_LAUNCH(k_inv_diag_long, nlong, kThreads, 0, s, A, G.g.piece, G.g.pbase, l1, omega, invm, bad_row);
 }
 
 __global__ void k_diag(Csr A, int l1, double* out) {

@@ -263,10 +263,48 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
 
 // ------------------------------------------------------------------ solve plan
 
+// Mapped pinned flag slots shared by all solve workspaces: one page pinned
+// once per process (pinned allocations are slow and synchronising; a
+// workspace is built per hierarchy).
+namespace {
+std::mutex g_slot_mu;
+int* g_slot_host = nullptr;
+int* g_slot_dev = nullptr;
+std::vector<int> g_slot_free;
+constexpr int kFlagSlots = 1024, kFlagStride = 4;
+}  // namespace
+int mapped_slot_acquire(int** host, int** dev) {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (!g_slot_host) {
+        UA_CK(cudaHostAlloc((void**)&g_slot_host, sizeof(int) * kFlagSlots * kFlagStride, cudaHostAllocMapped));
+        UA_CK(cudaHostGetDevicePointer((void**)&g_slot_dev, g_slot_host, 0));
+        for (int k = kFlagSlots - 1; k >= 0; --k) g_slot_free.push_back(k);
+    }
+    if (g_slot_free.empty()) throw Error(UAAMG_ECUDA, "too many live solve workspaces (mapped flag slots)");
+    const int k = g_slot_free.back();
+    g_slot_free.pop_back();
+    *host = g_slot_host + k * kFlagStride;
+    *dev = g_slot_dev + k * kFlagStride;
+    return k;
+}
+void mapped_slot_release(int k) {
+    if (k < 0) return;
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    g_slot_free.push_back(k);
+}
+
 std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, bool engine,
                                   int mat_levels) {
     std::unique_ptr<SolveWs> ws(new SolveWs());
     ws->key = p;
+    static const bool wsprof = getenv("UAAMG_WS_PROF") != nullptr;  // diagnostics
+    double wlast = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    auto wmark = [&](const char* what) {
+        if (!wsprof) return;
+        const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        fprintf(stderr, "  ws %-12s %.3f ms\n", what, t - wlast);
+        wlast = t;
+    };
     const int nl = (int)h->levels.size();
     ws->lev.resize(nl);
     ws->fcg.alloc(nl, s);
@@ -279,11 +317,20 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
     ws->sums.alloc(4 * nl + 4, s);
     ws->err.alloc(1, s);
     UA_CK(cudaMemsetAsync(ws->err.p, 0, sizeof(int), s));
-    ws->bad_row.alloc(1, s);
+    ws->bad_row.alloc(nl, s);
+    {
+        std::vector<int> init(nl, 0x7fffffff);
+        UA_CK(cudaMemcpyAsync(ws->bad_row.p, init.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s));
+        UA_CK(cudaStreamSynchronize(s));  // host vector is a temporary
+    }
     ws->fpart.alloc(2 * (size_t)kNumSMs * 8, s);
     ws->fbar.alloc(2, s);
     UA_CK(cudaMemsetAsync(ws->fbar.p, 0, 2 * sizeof(unsigned), s));
     const bool sing = h->singular;
+    if (wsprof) {
+        UA_CK(cudaStreamSynchronize(s));
+        wmark("prior-work");
+    }
     for (int l = 0; l < nl; ++l) {
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
@@ -301,25 +348,34 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
             W.p0.alloc(n, s); W.p1.alloc(n, s); W.ap0.alloc(n, s); W.ap1.alloc(n, s);
         }
         // smoother diagonal, hoisted out of the cycle (the reference
-        // recomputes it per smooth() call with identical values)
-        int h_bad = 0x7fffffff;
-        UA_CK(cudaMemcpyAsync(ws->bad_row.p, &h_bad, sizeof(int), cudaMemcpyHostToDevice, s));
-        launch_inv_diag(L.csr(), p.smoother_l1, p.omega, W.invm.p, ws->bad_row.p, s);
-        UA_CK(cudaMemcpyAsync(&h_bad, ws->bad_row.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        UA_CK(cudaStreamSynchronize(s));
-        if (h_bad != 0x7fffffff) {
-            throw Error(UAAMG_ENUMERICAL, "non-positive smoother diagonal at row " + std::to_string(h_bad));
-        }
+        // recomputes it per smooth() call with identical values); the
+        // first bad row of each level is checked after the loop (one sync)
+        launch_inv_diag(L.csr(), L.grp, p.smoother_l1, p.omega, W.invm.p, ws->bad_row.p + l, s);
     }
+    wmark("levels");
+    if (wsprof) {
+        UA_CK(cudaStreamSynchronize(s));
+        wmark("levels-gpu");
+    }
+    {
+        std::vector<int> hb(nl);
+        UA_CK(cudaMemcpyAsync(hb.data(), ws->bad_row.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        for (int l = 0; l < nl - 1; ++l)  // the reference's smooth() order: finest level first
+            if (hb[l] != 0x7fffffff)
+                throw Error(UAAMG_ENUMERICAL, "non-positive smoother diagonal at row " + std::to_string(hb[l]));
+    }
+    wmark("diag-check");
     const size_t n0 = h->levels[0]->n;
     ws->r.alloc(n0, s); ws->z.alloc(n0, s); ws->p0.alloc(n0, s); ws->p1.alloc(n0, s);
     ws->ap0.alloc(n0, s); ws->ap1.alloc(n0, s); ws->bproj.alloc(n0, s);
     ws->hist.alloc((size_t)p.max_iters + 1, s);
-    UA_CK(cudaHostAlloc(&ws->h_flags, 4 * sizeof(int), cudaHostAllocMapped));
-    UA_CK(cudaHostGetDevicePointer((void**)&ws->d_flags, ws->h_flags, 0));
+    wmark("outer-alloc");
+    ws->flag_slot = mapped_slot_acquire(&ws->h_flags, &ws->d_flags);
     UA_CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     UA_CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
+    wmark("outer");
     // persistent coarse engine from the first level (>= 1) small enough
     const long long erows = p.engine_rows < 0 ? kEngDefaultRows : p.engine_rows;
     ws->Lc = -1;
@@ -358,6 +414,7 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         UA_CK(cudaMemsetAsync(ws->ebar.p, 0, 2 * sizeof(unsigned), s));
         UA_CK(cudaStreamSynchronize(s));  // ops vector is a host temporary
     }
+    wmark("engine");
     // the level above the coarsest as one cluster kernel (tail.cu)
     if (!getenv("UAAMG_NO_TAIL") && ws->Lc < 0 && !sing && nl >= 3 && p.pre_sweeps <= 1 && p.post_sweeps <= 1) {
         const int Lt = nl - 2;
@@ -387,7 +444,9 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         in.pre = p.pre_sweeps;
         in.post = p.post_sweeps;
         in.steps = (!p.kcycle || p.inner_krylov_steps == 0) ? 0 : p.inner_krylov_steps;
+        wmark("tail-d2h");
         if (build_tail(in, ws->tail, s)) ws->tail.Lt = Lt;
+        wmark("tail-build");
     }
     ws->ready = true;
     UA_CK(cudaStreamSynchronize(s));
@@ -443,7 +502,13 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     std::lock_guard<std::mutex> lk(h->mu);
     StreamJoin join(s, h->stream);
     s = h->stream;
+    static const bool wsprof = getenv("UAAMG_WS_PROF") != nullptr;  // diagnostics
+    auto wall = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double w0 = wsprof ? wall() : 0.0;
     ensure_ws(h, p, s);
+    if (wsprof) fprintf(stderr, "solve ws build %.3f ms\n", wall() - w0);
     SolveWs* ws = h->ws.get();
     Plan pl{h, ws, p, s};
     Level& L = *h->levels[0];
@@ -490,8 +555,10 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     UA_CK(cudaStreamSynchronize(s));
     if (hst.bnorm == 0.0) UA_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));  // U/solvers.py:206-207
     if (p.use_graphs && (!ws->graphs_built || ws->graph_x != x || ws->profiled != (p.profile_level0 != 0))) {
+        const double w1 = wsprof ? wall() : 0.0;
         build_graphs(pl, x);
         ws->graph_x = x;
+        if (wsprof) fprintf(stderr, "solve graph capture+instantiate %.3f ms\n", wall() - w1);
     }
     int launched = 0;
     int64_t prof_n = 0;

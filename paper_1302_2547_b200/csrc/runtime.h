@@ -45,6 +45,9 @@ struct LevelWs {
     DBuf<double> xf, rf, z, p0, p1, ap0, ap1;                // inner FCG
 };
 
+int mapped_slot_acquire(int** host, int** dev);
+void mapped_slot_release(int k);
+
 struct SolveWs {
     uaamg_solve_params key{};
     bool ready = false;
@@ -83,12 +86,13 @@ struct SolveWs {
     double* graph_x = nullptr;  // graphs bake in the iterate pointer
     int* h_flags = nullptr;  // pinned, mapped: [0] mirror of NpcgState::active
     int* d_flags = nullptr;  // its device address
+    int flag_slot = -1;      // slot in the shared mapped page (mapped_slot_acquire)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     ~SolveWs() {
         for (auto& g : graph) if (g) cudaGraphExecDestroy(g);
         for (auto& row : pev)
             for (auto& e : row) if (e) cudaEventDestroy(e);
-        if (h_flags) cudaFreeHost(h_flags);
+        mapped_slot_release(flag_slot);
         for (auto& e : ev) if (e) cudaEventDestroy(e);
     }
 };

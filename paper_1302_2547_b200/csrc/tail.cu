@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "csr_tma.cuh"
 #include "tail.h"
@@ -848,7 +849,11 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
         UA_CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax));
         attr_done = true;
     }
-    {
+    static std::map<std::pair<int, int>, bool> fits_cache;  // (cs, smem) -> a cluster can be resident
+    auto fc = fits_cache.find({cs, L.smem_bytes});
+    if (fc != fits_cache.end()) {
+        if (!fc->second) return false;
+    } else {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(cs);
         lc.blockDim = dim3(kTailThreads);
@@ -861,10 +866,10 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
         lc.attrs = at;
         lc.numAttrs = 1;
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k_tail, &lc) != cudaSuccess || ncl < 1) {
-            (void)cudaGetLastError();
-            return false;
-        }
+        const bool ok = cudaOccupancyMaxActiveClusters(&ncl, k_tail, &lc) == cudaSuccess && ncl >= 1;
+        if (!ok) (void)cudaGetLastError();
+        fits_cache[{cs, L.smem_bytes}] = ok;
+        if (!ok) return false;
     }
     TailArgs& a = tp.args;
     a = TailArgs{};
