@@ -273,6 +273,28 @@ int* g_slot_dev = nullptr;
 std::vector<int> g_slot_free;
 constexpr int kFlagSlots = 1024, kFlagStride = 4;
 }  // namespace
+// Executable iteration graphs of released workspaces (bench-style loops build
+// a hierarchy of the same shape per step; cudaGraphExecUpdate on a cached
+// exec is much cheaper than a fresh instantiation).
+namespace {
+std::mutex g_graph_mu;
+std::vector<cudaGraphExec_t> g_graph_cache;
+constexpr size_t kGraphCacheMax = 4;
+}  // namespace
+cudaGraphExec_t graph_cache_take() {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graph_cache.empty()) return nullptr;
+    cudaGraphExec_t e = g_graph_cache.back();
+    g_graph_cache.pop_back();
+    return e;
+}
+void graph_cache_give(cudaGraphExec_t e) {
+    if (!e) return;
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graph_cache.size() < kGraphCacheMax) g_graph_cache.push_back(e);
+    else cudaGraphExecDestroy(e);
+}
+
 int mapped_slot_acquire(int** host, int** dev) {
     std::lock_guard<std::mutex> lk(g_slot_mu);
     if (!g_slot_host) {
@@ -483,8 +505,26 @@ static void build_graphs(Plan& pl, double* x) {
         // captured launches are not executions: account them per replay
         ws->graph_kernels[par] = g_launches.load() - before;
         g_launches.fetch_sub(ws->graph_kernels[par]);
+        static const bool gprof = getenv("UAAMG_WS_PROF") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         if (ws->graph[par]) cudaGraphExecDestroy(ws->graph[par]);
-        UA_CK(cudaGraphInstantiate(&ws->graph[par], g, 0));
+        ws->graph[par] = nullptr;
+        // a released workspace's executable graph of the same topology (a new
+        // hierarchy of the same shape) is re-pointed instead of re-instantiated
+        cudaGraphExec_t reuse = graph_cache_take();
+        if (reuse) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(reuse, g, &info) == cudaSuccess) {
+                ws->graph[par] = reuse;
+            } else {
+                (void)cudaGetLastError();
+                cudaGraphExecDestroy(reuse);
+            }
+        }
+        if (!ws->graph[par]) UA_CK(cudaGraphInstantiate(&ws->graph[par], g, 0));
+        if (gprof)
+            fprintf(stderr, "  graph %d %s %.3f ms\n", par, reuse && ws->graph[par] == reuse ? "update" : "instantiate",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         cudaGraphDestroy(g);
     }
     ws->graphs_built = true;

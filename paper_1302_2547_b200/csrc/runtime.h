@@ -47,6 +47,8 @@ struct LevelWs {
 
 int mapped_slot_acquire(int** host, int** dev);
 void mapped_slot_release(int k);
+cudaGraphExec_t graph_cache_take();
+void graph_cache_give(cudaGraphExec_t e);
 
 struct SolveWs {
     uaamg_solve_params key{};
@@ -89,7 +91,7 @@ struct SolveWs {
     int flag_slot = -1;      // slot in the shared mapped page (mapped_slot_acquire)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     ~SolveWs() {
-        for (auto& g : graph) if (g) cudaGraphExecDestroy(g);
+        for (auto& g : graph) graph_cache_give(g);  // the work using it has completed
         for (auto& row : pev)
             for (auto& e : row) if (e) cudaEventDestroy(e);
         mapped_slot_release(flag_slot);
