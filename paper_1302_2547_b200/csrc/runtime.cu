@@ -396,6 +396,7 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
     ws->flag_slot = mapped_slot_acquire(&ws->h_flags, &ws->d_flags);
     UA_CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     UA_CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
+    for (auto& e : ws->evr) UA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
     wmark("outer");
     // persistent coarse engine from the first level (>= 1) small enough
@@ -615,7 +616,22 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
         }
         ++prof_n;
     };
-    if (hst.active) {
+    if (hst.active && !prof && p.use_graphs) {
+        // Pipelined kLookahead iterations deep: iteration it is launched
+        // before iteration it-kLookahead's decision is read, so a host stall
+        // shorter than that many iterations never idles the GPU; at most
+        // kLookahead gated no-op replays run past convergence.
+        for (int it = 0; it < p.max_iters; ++it) {
+            UA_CK(cudaGraphLaunch(ws->graph[it & 1], s));
+            g_launches.fetch_add(ws->graph_kernels[it & 1]);
+            ++launched;
+            UA_CK(cudaEventRecord(ws->evr[it % kEvRing], s));
+            if (it >= kLookahead) {
+                UA_CK(cudaEventSynchronize(ws->evr[(it - kLookahead) % kEvRing]));
+                if (*(volatile int*)ws->h_flags == 0) break;  // decision of >= iteration it - kLookahead
+            }
+        }
+    } else if (hst.active) {
         // Pipelined: iteration it is launched before iteration it-1's
         // "active" flag is read, so at most one gated no-op replay runs past
         // convergence.  `before[par]`: was the solve active when the replay of

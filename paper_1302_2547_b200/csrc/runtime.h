@@ -45,6 +45,8 @@ struct LevelWs {
     DBuf<double> xf, rf, z, p0, p1, ap0, ap1;                // inner FCG
 };
 
+constexpr int kLookahead = 3;  // iteration graphs queued ahead of the host's flag read
+constexpr int kEvRing = 4;
 int mapped_slot_acquire(int** host, int** dev);
 void mapped_slot_release(int k);
 cudaGraphExec_t graph_cache_take();
@@ -90,12 +92,14 @@ struct SolveWs {
     int* d_flags = nullptr;  // its device address
     int flag_slot = -1;      // slot in the shared mapped page (mapped_slot_acquire)
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEvent_t evr[4] = {nullptr, nullptr, nullptr, nullptr};  // lookahead ring (kEvRing)
     ~SolveWs() {
         for (auto& g : graph) graph_cache_give(g);  // the work using it has completed
         for (auto& row : pev)
             for (auto& e : row) if (e) cudaEventDestroy(e);
         mapped_slot_release(flag_slot);
         for (auto& e : ev) if (e) cudaEventDestroy(e);
+        for (auto& e : evr) if (e) cudaEventDestroy(e);
     }
 };
 
