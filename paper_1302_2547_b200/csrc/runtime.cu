@@ -648,9 +648,6 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
             }
             ++launched;
             last_par = par;
-            static const bool flag_copy = getenv("UAAMG_FLAG_COPY") != nullptr;  // A/B diagnostics
-            if (flag_copy)
-                UA_CK(cudaMemcpyAsync(ws->h_flags, &ws->npcg.p->active, sizeof(int), cudaMemcpyDeviceToHost, s));
             UA_CK(cudaEventRecord(ws->ev[par], s));
             if (it >= 1) {
                 UA_CK(cudaEventSynchronize(ws->ev[par ^ 1]));

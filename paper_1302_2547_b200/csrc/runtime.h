@@ -241,7 +241,6 @@ struct Plan {
             double* o = direct ? C.e.p : C.xf.p;
             int* u0 = direct ? nullptr : &ws->fcg.p[l + 1].upd[0];
             launch_tail(ws->tail, W.r.p, gate, o, u0, s);
-            if (getenv("UAAMG_TAIL_TWICE")) launch_tail(ws->tail, W.r.p, gate, o, u0, s);
             ec = o;
             ec_valid = u0;
         } else if (l + 1 == ws->Lc) {

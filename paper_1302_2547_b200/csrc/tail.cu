@@ -933,8 +933,7 @@ void launch_tail(const TailPlan& tp, const double* rprev, const int* gate, doubl
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    static const bool no_pdl = getenv("UAAMG_TAIL_NOPDL") != nullptr;  // diagnostics
-    cfg.numAttrs = no_pdl ? 1 : 2;
+    cfg.numAttrs = 2;
     UA_CK(cudaLaunchKernelEx(&cfg, k_tail, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
