@@ -7,6 +7,7 @@
 // Reference: U/aggregation.py:130-203, U/hierarchy.py:22-65,
 // K/numba_backend.py:14-44 (hash), :100-111 (scores), :145-273.
 #include <cooperative_groups.h>
+#include <chrono>
 #include <cstring>
 #include <cub/cub.cuh>
 
@@ -114,7 +115,8 @@ __global__ void k_select(Csr A, const double* __restrict__ s, uint8_t* st, const
             ++local;
         }
     }
-    if (local) atomicAdd(n_centers, local);
+    local = __reduce_add_sync(0xffffffffu, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_centers, local);
 }
 
 // hop 2, claim (K/numba_backend.py:196-220): owner = best center within
@@ -195,7 +197,7 @@ __global__ void k_admit_step(Csr A, const int* __restrict__ owner, uint8_t* adm,
             }
         }
     }
-    if (local) atomicOr(changed, 1);
+    if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
 }
 // commit: admitted vertices and centers become processed with their seed
 __global__ void k_admit_commit(int n, uint8_t* st, const int* owner, const uint8_t* adm, int* seed_of,
@@ -210,7 +212,8 @@ __global__ void k_admit_commit(int n, uint8_t* st, const int* owner, const uint8
             ++local;
         }
     }
-    if (local) atomicAdd(remaining, local);
+    local = __reduce_add_sync(0xffffffffu, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(remaining, local);
 }
 
 // Capped: per-center sequential greedy exactly as the reference (bucket in
@@ -295,7 +298,8 @@ __global__ void k_capped_commit(int n, uint8_t* st, uint8_t* newly, int* remaini
         if (st[j] == 1 || newly[j]) { st[j] = 2; newly[j] = 0; }
         else if (st[j] == 0) ++local;
     }
-    if (local) atomicAdd(remaining, local);
+    local = __reduce_add_sync(0xffffffffu, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(remaining, local);
 }
 
 // ============================================================ cooperative aggregation
@@ -490,8 +494,15 @@ struct ClusterBar {
 };
 constexpr int kAggClusterThreads = 1024;
 constexpr int kAggClusterCtas = 16;
-constexpr int kAggClusterMaxRows = 65536;  // levels up to this size aggregate on one cluster
+constexpr int kAggClusterMaxRows = 32768;  // levels up to this size aggregate on one cluster (measured: C2 L2, 42404 rows, faster on the grid)
 
+// UAAMG_AGG_PROF: globaltimer after each phase barrier of passes 0-1
+#define AGG_STAMP(K)                                                          \
+    if (g.prof && pass < 2 && tid == 0) {                                     \
+        unsigned long long tt;                                                \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                \
+        g.prof[140 + pass * 16 + (K)] = tt;                                   \
+    }
 template <class Bar>
 __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
     const Bar grid{};
@@ -535,13 +546,16 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             }
         }
         grid.sync();
+        AGG_STAMP(0);
         if (U.list) {
             wl_compact(g.mark, stamp, n, g.hlist, hcnt, tid, nth);
             grid.sync();
+            AGG_STAMP(1);
             H = WL{g.hlist, ctl[14 + (pass & 1)]};
         }
         coop_hop1(g, H, 0, stamp, nlong, tid, nth, lane, w, nw);
         grid.sync();
+        AGG_STAMP(2);
         // selection (K/numba_backend.py:175-193)
         int local = 0;
         for (int t = tid; t < U.cnt; t += nth) {
@@ -563,10 +577,15 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             warp_keymax(bs, bi);
             if (lane == 0 && (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi))) { g.st[i] = 1; ++local; }
         }
-        if (local) atomicAdd((int*)&ctl[ps], local);
+        // one atomic per warp: per-thread same-address atomics serialise in L2
+        // (~300K of them at level 0 cost ~100 us per phase)
+        local = __reduce_add_sync(0xffffffffu, local);
+        if (lane == 0 && local) atomicAdd((int*)&ctl[ps], local);
         grid.sync();
+        AGG_STAMP(3);
         coop_hop1(g, H, 1, stamp, nlong, tid, nth, lane, w, nw);
         grid.sync();
+        AGG_STAMP(4);
         // claim (K/numba_backend.py:196-220) + admission seeds
         for (int t = tid; t < U.cnt; t += nth) {
             const int j = U[t];
@@ -592,6 +611,7 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             if (lane == 0) g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
         }
         grid.sync();
+        AGG_STAMP(5);
         // admission fixpoint (uncapped sweeps of K/numba_backend.py:235-273)
         // Plain (L1-cacheable) reads: a read may miss an admission made in
         // the same sweep, which only defers it to the next sweep -- the
@@ -641,8 +661,9 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
                 }
                 if (__any_sync(0xffffffffu, f) && lane == 0) { adm[j] = 1; ch = 1; }
             }
-            if (ch) atomicOr((int*)&ctl[6 + slot], 1);
+            if (__any_sync(0xffffffffu, ch) && lane == 0) atomicOr((int*)&ctl[6 + slot], 1);
             grid.sync();
+            AGG_STAMP(6);
             const int any = ctl[6 + slot];
             ++itg;
             if (!any) break;
@@ -657,11 +678,14 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             if (sj == 1 || (sj == 0 && adm[j])) { g.seed_of[j] = g.owner[j]; g.st[j] = 2; }
             else if (sj == 0) ++left;
         }
-        if (left) atomicAdd((int*)&ctl[3 + ps], left);
+        left = __reduce_add_sync(0xffffffffu, left);
+        if (lane == 0 && left) atomicAdd((int*)&ctl[3 + ps], left);
         grid.sync();
+        AGG_STAMP(7);
         if (ctl[3 + ps] > 0) {
             wl_compact_st(g.st, n, unext, ucnt, tid, nth);
             grid.sync();
+            AGG_STAMP(8);
         }
         if (g.prof && tid == 0 && pass < 32) {
             g.prof[4 * pass + 2] = H.cnt;
@@ -714,14 +738,19 @@ __global__ void k_seg_starts(int n, int nc, const int* sorted_keys, int* ptr) {
 
 // ============================================================ Galerkin
 // stream length per aggregate: sum of its members' row lengths
-__global__ void k_stream_len(int nc, const int* agg_ptr, const int* members, const int* rp, int* slen) {
-    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
-        int s = 0;
-        for (int q = agg_ptr[I]; q < agg_ptr[I + 1]; ++q) {
-            const int m = members[q];
-            s += rp[m + 1] - rp[m];
-        }
-        slen[I] = s;
+// stream length of aggregate I = sum of its members' row lengths, row-parallel
+// (a thread walking a hub aggregate's thousands of members was 0.4 ms);
+// lanes of a warp adding to the same aggregate are merged into one atomic
+__global__ void k_stream_len(Csr A, const int* __restrict__ v2a, int* slen) {
+    const int lane = threadIdx.x & 31;
+    for (int r0 = blockIdx.x * blockDim.x + threadIdx.x - lane; r0 < A.n; r0 += gridDim.x * blockDim.x) {
+        const int r = r0 + lane;
+        const int I = r < A.n ? v2a[r] : -1;
+        const int len = r < A.n ? A.rp[r + 1] - A.rp[r] : 0;
+        const unsigned g = __match_any_sync(0xffffffffu, I);
+        int tot = 0;
+        for (unsigned mm = g; mm; mm &= mm - 1) tot += __shfl_sync(g, len, __ffs(mm) - 1);
+        if (I >= 0 && (__ffs(g) - 1) == lane) atomicAdd(slen + I, tot);
     }
 }
 
@@ -807,28 +836,78 @@ __device__ __forceinline__ void gal_insert_add(int* K, double* V, int cap, int J
     }
     atomicAdd(V + slot, a);
 }
-__global__ void k_galerkin_accum_int(Csr A, int nc, const int* __restrict__ v2a, const int* __restrict__ soff,
-                                     const int* __restrict__ slen, int* hkey, double* hval) {
-    // short rows: one thread per row; rows longer than kLongRow: one warp per row
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    for (int r = tid; r < A.n; r += nth) {
-        const int e0 = A.rp[r], e1 = A.rp[r + 1];
-        if (e1 - e0 > kLongRow) continue;
-        const int I = v2a[r];
-        const int cap = gal_cap(slen[I], nc);
-        int* K = hkey + 2 * (size_t)soff[I];
-        double* V = hval + 2 * (size_t)soff[I];
-        for (int e = e0; e < e1; ++e) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+// shared-memory variant: int64 sums (fp64 shared atomics are CAS spin loops;
+// integer-valued sums below 2^52 are exact either way)
+template <class T>
+__device__ __forceinline__ void gal_insert_add_s(int* K, T* V, int cap, int J, T a) {
+    unsigned slot = hslot(J, cap);
+    while (true) {
+        const int prev = atomicCAS(K + slot, -1, J);
+        if (prev == -1 || prev == J) break;
+        slot = (slot + 1 == (unsigned)cap) ? 0u : slot + 1;
     }
-    const int lane = threadIdx.x & 31, w = tid >> 5, nw = nth >> 5;
-    for (int r = w; r < A.n; r += nw) {
+    if constexpr (sizeof(T) == 4)
+        atomicAdd(V + slot, a);  // native shared-memory add
+    else
+        atomicAdd(reinterpret_cast<unsigned long long*>(V + slot), (unsigned long long)a);
+}
+__global__ void __launch_bounds__(256) k_galerkin_accum_int(Csr A, int nc, const int* __restrict__ v2a,
+                                                            const int* __restrict__ soff,
+                                                            const int* __restrict__ slen, int* hkey, double* hval,
+                                                            const int* __restrict__ longs, const int* __restrict__ nlong) {
+    // short rows: one lane per row, the warp stepping through its rows'
+    // entries together; lanes hitting the same (I, J) in a step are merged
+    // (__match_any_sync) and one atomic adds their sum -- hub aggregates
+    // otherwise serialise thousands of same-address atomics in L2.  Rows
+    // longer than kLongRow: one warp per row, merged the same way.  Exact for
+    // integer values in any grouping.
+    __shared__ double wv[8][32];
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, w = tid >> 5, nw = nth >> 5;
+    auto merged_add = [&](bool act, int I, int J, double a) {
+        const unsigned long long key = act ? ((unsigned long long)(unsigned)I << 32 | (unsigned)J) : ~0ull;
+        const unsigned g = __match_any_sync(0xffffffffu, key);
+        wv[wib][lane] = a;
+        __syncwarp();
+        if (act && (__ffs(g) - 1) == lane) {
+            double sum = 0.0;
+            for (unsigned mm = g; mm; mm &= mm - 1) sum += wv[wib][__ffs(mm) - 1];
+            gal_insert_add(hkey + 2 * (size_t)soff[I], hval + 2 * (size_t)soff[I], gal_cap(slen[I], nc), J, sum);
+        }
+        __syncwarp();
+    };
+    for (int r0 = tid - lane; r0 < A.n; r0 += nth) {
+        const int r = r0 + lane;
+        int e0 = 0, len = 0, I = 0;
+        if (r < A.n) {
+            e0 = A.rp[r];
+            len = A.rp[r + 1] - e0;
+            if (len > kLongRow) len = 0;
+            I = v2a[r];
+        }
+        const int mx = __reduce_max_sync(0xffffffffu, len);
+        for (int k = 0; k < mx; ++k) {
+            const bool act = k < len;
+            const int J = act ? __ldg(v2a + __ldg(A.ci + e0 + k)) : -1;
+            const double a = act ? __ldg(A.av + e0 + k) : 0.0;
+            merged_add(act, I, J, a);
+        }
+    }
+    // long rows (listed by k_long_rows): chunks of 32 entries spread over
+    // all warps -- a hub row of thousands of entries walked by one warp is a
+    // serial chain of dependent gathers and atomics
+    const int nl = *nlong;
+    for (int li = 0; li < nl; ++li) {
+        const int r = longs[li];
         const int e0 = A.rp[r], e1 = A.rp[r + 1];
-        if (e1 - e0 <= kLongRow) continue;
         const int I = v2a[r];
-        const int cap = gal_cap(slen[I], nc);
-        int* K = hkey + 2 * (size_t)soff[I];
-        double* V = hval + 2 * (size_t)soff[I];
-        for (int e = e0 + lane; e < e1; e += 32) gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+        const int nch = (e1 - e0 + 31) >> 5;
+        // rotate the starting warp per row so short lists still spread
+        for (int c = (w + li * 7) % nw; c < nch; c += nw) {
+            const int e = e0 + (c << 5) + lane;
+            const bool act = e < e1;
+            merged_add(act, I, act ? __ldg(v2a + __ldg(A.ci + e)) : -1, act ? __ldg(A.av + e) : 0.0);
+        }
     }
 }
 // Integer path on levels whose aggregate streams are all short (fine
@@ -842,6 +921,7 @@ __global__ void k_galerkin_accum_int(Csr A, int nc, const int* __restrict__ v2a,
 constexpr int kGalWarps = 8;
 constexpr int kGalStreamMax = 256;          // levels whose longest stream is longer take the global tables
 constexpr int kGalCap = 2 * kGalStreamMax;  // shared-memory table slots per warp (load <= 1/2)
+template <class T>  // int when every stream's |sum| < 2^31 (native atomics), else long long
 __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int nc, const int* __restrict__ v2a,
                                                                      const int* __restrict__ agg_ptr,
                                                                      const int* __restrict__ members,
@@ -849,7 +929,7 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
                                                                      const int* __restrict__ slen, int* tk,
                                                                      double* tv, int* cnt) {
     __shared__ int sk[kGalWarps][kGalCap];
-    __shared__ double sv[kGalWarps][kGalCap];
+    __shared__ T sv[kGalWarps][kGalCap];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int I = blockIdx.x * kGalWarps + wib; I < nc; I += gridDim.x * kGalWarps) {
         const int L = slen[I];
@@ -857,10 +937,10 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
         int cap = 32;
         while (cap < need) cap <<= 1;  // <= kGalCap on this path (every stream <= kGalStreamMax)
         int* K = sk[wib];
-        double* V = sv[wib];
+        T* V = sv[wib];
         for (int t = lane; t < cap; t += 32) {
             K[t] = -1;
-            V[t] = 0.0;
+            V[t] = 0;
         }
         __syncwarp();
         const int m0 = agg_ptr[I], m1 = agg_ptr[I + 1];
@@ -889,7 +969,7 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
                 const int exj = __shfl_sync(0xffffffffu, excl, j);
                 if (sidx < total) {
                     const int e = rbj + (sidx - exj);
-                    gal_insert_add(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), __ldg(A.av + e));
+                    gal_insert_add_s(K, V, cap, __ldg(v2a + __ldg(A.ci + e)), (T)__ldg(A.av + e));
                 }
             }
         }
@@ -902,7 +982,7 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
             double v = 0.0;
             if (t < cap) {
                 key = K[t];
-                v = V[t];
+                v = (double)V[t];
             }
             const bool keep = key >= 0 && v != 0.0;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -1235,8 +1315,8 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         DBuf<unsigned long long> prof;
         g.prof = nullptr;
         if (aprof) {
-            prof.alloc(4 * 33, s);
-            UA_CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * 4 * 33, s));
+            prof.alloc(4 * 33 + 40, s);
+            UA_CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * (4 * 33 + 40), s));
             g.prof = prof.p;
         }
         static int max_blocks = 0;
@@ -1251,7 +1331,9 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         // latency-bound, fewer CTAs (cheaper barriers) measured slower
         int blocks = std::max(1, std::min(max_blocks, cdiv(n, 256)));
         static const bool no_cluster = getenv("UAAMG_AGG_NO_CLUSTER") != nullptr;  // A/B diagnostics
-        if (n <= kAggClusterMaxRows && !no_cluster) {
+        static const int cl_max = getenv("UAAMG_AGG_CLUSTER_MAX") ? atoi(getenv("UAAMG_AGG_CLUSTER_MAX"))
+                                                                  : kAggClusterMaxRows;  // A/B diagnostics
+        if (n <= cl_max && !no_cluster) {
             // small level: every pass is a chain of latency-bound phases;
             // one 16-CTA cluster with hardware barriers instead of the grid
             static bool attr = false;
@@ -1283,8 +1365,19 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         remaining = h_cnt[1];
         max_passes = 0;  // skip the host-driven loop below
         if (aprof) {
-            unsigned long long hp[4 * 33];
+            unsigned long long hp[4 * 33 + 40];
             UA_CK(cudaMemcpy(hp, prof.p, sizeof(hp), cudaMemcpyDeviceToHost));
+            for (int ps = 0; ps < 2; ++ps) {
+                fprintf(stderr, "  pass %d phases (us):", ps);
+                unsigned long long prev = hp[4 * ps];
+                for (int q = 0; q < 16; ++q) {
+                    const unsigned long long v = hp[140 + ps * 16 + q];
+                    if (!v) continue;
+                    fprintf(stderr, " %d:%.1f", q, (v - prev) * 1e-3);
+                    prev = v;
+                }
+                fprintf(stderr, "\n");
+            }
             fprintf(stderr, "aggregate n=%d blocks=%d passes=%d\n", n, blocks, passes);
             for (int k = 0; k < std::min(passes, 32); ++k)
                 fprintf(stderr, "  pass %2d |U| %9llu |H| %9llu adm-it %2llu  %8.1f us\n", k, hp[4 * k + 1],
@@ -1351,7 +1444,8 @@ void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cu
 }
 
 // true when every value is an integer and nnz * max|a| < 2^52 (exact in any order)
-static bool integer_exact(const Csr& A, cudaStream_t s) {
+static bool integer_exact(const Csr& A, cudaStream_t s, double* maxabs = nullptr) {
+    if (maxabs) *maxabs = 0.0;
     if (A.nnz == 0) return true;
     DBuf<int> bad(1, s);
     DBuf<unsigned long long> mx(1, s);
@@ -1365,20 +1459,35 @@ static bool integer_exact(const Csr& A, cudaStream_t s) {
     UA_CK(cudaStreamSynchronize(s));
     double m;
     std::memcpy(&m, &h_mx, 8);
+    if (maxabs) *maxabs = m;
     return h_bad == 0 && (double)A.nnz * m < 4503599627370496.0;  // 2^52
 }
 
 // Galerkin: returns nnz_c; allocates out arrays
 long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
                           DBuf<int>& rp_c, DBuf<int>& ci_c, DBuf<double>& av_c, cudaStream_t s) {
+    static const bool gprof = getenv("UAAMG_GAL_PROF") != nullptr;  // diagnostics: per-step stream time
+    auto gt = [&](const char* tag) {
+        if (!gprof) return;
+        static auto last = std::chrono::steady_clock::now();
+        UA_CK(cudaStreamSynchronize(s));
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "  galerkin nc=%d %-10s %8.3f ms\n", nc, tag, std::chrono::duration<double, std::milli>(now - last).count());
+        last = now;
+    };
+    gt("start");
     DBuf<int> slen(nc + 1, s), soff(nc + 1, s), cnt(nc + 1, s);
-    UA_LAUNCH(k_stream_len, grid_for(nc), 256, 0, s, nc, agg_ptr, members, A.rp, slen.p);
+    UA_CK(cudaMemsetAsync(slen.p, 0, sizeof(int) * nc, s));
+    UA_LAUNCH(k_stream_len, grid_for(A.n), 256, 0, s, A, v2a, slen.p);
     UA_CK(cudaMemsetAsync(slen.p + nc, 0, sizeof(int), s));
     exclusive_scan(slen.p, soff.p, nc + 1, s);
+    gt("slen");
     const size_t hsz = 2 * (size_t)std::max(A.nnz, 1);
     SPtr<int> hkey{scratch<int>(0, hsz)};
     SPtr<double> hval{scratch<double>(1, hsz)};
-    const bool exact_int = integer_exact(A, s);
+    double maxabs = 0.0;
+    const bool exact_int = integer_exact(A, s, &maxabs);
+    gt("intcheck");
     SPtr<int> tk{nullptr};
     SPtr<double> tv{nullptr};
     // warp-per-aggregate shared-memory tables when every aggregate's stream
@@ -1400,13 +1509,23 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     if (exact_int && !warp_path) {
         UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
         UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
-        UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, nc, v2a, soff.p, slen.p, hkey.p, hval.p);
+        DBuf<int> nlong(1, s);
+        SPtr<int> longs{scratch<int>(13, (size_t)std::max(A.n, 1))};
+        UA_CK(cudaMemsetAsync(nlong.p, 0, sizeof(int), s));
+        UA_LAUNCH(k_long_rows, grid_for(A.n), 256, 0, s, A, longs.p, nlong.p);
+        UA_LAUNCH(k_galerkin_accum_int, grid_for(A.n), 256, 0, s, A, nc, v2a, soff.p, slen.p, hkey.p, hval.p,
+                  longs.p, nlong.p);
         UA_LAUNCH(k_galerkin_count, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, cnt.p);
     } else if (exact_int) {
         tk.p = scratch<int>(14, (size_t)std::max(A.nnz, 1));
         tv.p = scratch<double>(15, (size_t)std::max(A.nnz, 1));
-        UA_LAUNCH(k_galerkin_int_warp, std::min(cdiv(nc, kGalWarps), 148 * 16), 32 * kGalWarps, 0, s, A, nc, v2a,
-                  agg_ptr, members, soff.p, slen.p, tk.p, tv.p, cnt.p);
+        // every stream is <= kGalStreamMax entries of |a| <= maxabs
+        if ((double)kGalStreamMax * maxabs < 2147483647.0)
+            UA_LAUNCH(k_galerkin_int_warp<int>, std::min(cdiv(nc, kGalWarps), 148 * 16), 32 * kGalWarps, 0, s, A, nc,
+                      v2a, agg_ptr, members, soff.p, slen.p, tk.p, tv.p, cnt.p);
+        else
+            UA_LAUNCH(k_galerkin_int_warp<long long>, std::min(cdiv(nc, kGalWarps), 148 * 16), 32 * kGalWarps, 0, s, A,
+                      nc, v2a, agg_ptr, members, soff.p, slen.p, tk.p, tv.p, cnt.p);
 
     } else {
         UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
@@ -1414,12 +1533,14 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
         UA_LAUNCH(k_galerkin_accum, cdiv(nc, 8), 256, 0, s, A, v2a, nc, agg_ptr, members, soff.p, slen.p, hkey.p,
                   hval.p, cnt.p);
     }
+    gt("accum");
     UA_CK(cudaMemsetAsync(cnt.p + nc, 0, sizeof(int), s));
     rp_c.alloc(nc + 1, s);
     exclusive_scan(cnt.p, rp_c.p, nc + 1, s);
     int nnz_c = 0;
     UA_CK(cudaMemcpyAsync(&nnz_c, rp_c.p + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
+    gt("scan");
     ci_c.alloc(std::max(nnz_c, 1), s);
     av_c.alloc(std::max(nnz_c, 1), s);
     if (nnz_c > 0) {
@@ -1438,6 +1559,7 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
         UA_CK(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
                                                   rp_c.p + 1, s));
     }
+    gt("sort");
     return nnz_c;
 }
 
