@@ -465,13 +465,54 @@ __device__ __forceinline__ void wl_append(bool f, int k, int* list, int* cnt) {
     b = __shfl_sync(0xffffffffu, b, 0);
     if (f) list[b + __popc(m & ((1u << lane) - 1u))] = k;
 }
-__device__ void wl_compact(const int* mark, int stamp, int n, int* list, int* cnt, int tid, int nth) {
-    const int n32 = (n + 31) & ~31;  // whole warps iterate together
-    for (int k = tid; k < n32; k += nth) wl_append(k < n && mark[k] == stamp, k, list, cnt);
+// block-aggregated compaction: each thread tests 4 consecutive vertices, a
+// block scan places them and ONE atomic per block tile reserves the range
+// (one atomic per warp was ~65K same-address atomics at level 0, ~45 us)
+template <class Pred>
+__device__ void wl_compact_blk(int n, Pred pred, int* list, int* cnt) {
+    __shared__ int wsum[32];
+    __shared__ int bbase;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int tile = blockDim.x * 4;
+    for (int base = blockIdx.x * tile; base < n; base += gridDim.x * tile) {
+        const int k0 = base + threadIdx.x * 4;
+        unsigned bits = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (k0 + q < n && pred(k0 + q)) bits |= 1u << q;
+        const int c = __popc(bits);
+        int x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wib] = x;
+        __syncthreads();
+        if (wib == 0) {
+            int v = lane < nwb ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            if (lane < nwb) wsum[lane] = v;  // inclusive
+            const int tot = __shfl_sync(0xffffffffu, v, 31);
+            if (lane == 0) bbase = tot ? atomicAdd(cnt, tot) : 0;
+        }
+        __syncthreads();
+        int off = bbase + (wib ? wsum[wib - 1] : 0) + x - c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (bits >> q & 1u) list[off++] = k0 + q;
+        __syncthreads();
+    }
 }
-__device__ void wl_compact_st(const uint8_t* st, int n, int* list, int* cnt, int tid, int nth) {
-    const int n32 = (n + 31) & ~31;
-    for (int k = tid; k < n32; k += nth) wl_append(k < n && st[k] == 0, k, list, cnt);
+__device__ void wl_compact(const int* mark, int stamp, int n, int* list, int* cnt, int, int) {
+    wl_compact_blk(n, [&](int k) { return mark[k] == stamp; }, list, cnt);
+}
+__device__ void wl_compact_st(const uint8_t* st, int n, int* list, int* cnt, int, int) {
+    wl_compact_blk(n, [&](int k) { return st[k] == 0; }, list, cnt);
 }
 
 // rows longer than kLongRow, appended in any order
