@@ -468,18 +468,20 @@ __device__ __forceinline__ void wl_append(bool f, int k, int* list, int* cnt) {
 // block-aggregated compaction: each thread tests 4 consecutive vertices, a
 // block scan places them and ONE atomic per block tile reserves the range
 // (one atomic per warp was ~65K same-address atomics at level 0, ~45 us)
-template <class Pred>
-__device__ void wl_compact_blk(int n, Pred pred, int* list, int* cnt) {
+// items t in [0, m): f(t, v) says whether to append v (called once per item)
+template <class F>
+__device__ void wl_compact_blk(int m, F f, int* list, int* cnt) {
     __shared__ int wsum[32];
     __shared__ int bbase;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int tile = blockDim.x * 4;
-    for (int base = blockIdx.x * tile; base < n; base += gridDim.x * tile) {
+    for (int base = blockIdx.x * tile; base < m; base += gridDim.x * tile) {
         const int k0 = base + threadIdx.x * 4;
         unsigned bits = 0;
+        int vals[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (k0 + q < n && pred(k0 + q)) bits |= 1u << q;
+            if (k0 + q < m && f(k0 + q, vals[q])) bits |= 1u << q;
         const int c = __popc(bits);
         int x = c;
 #pragma unroll
@@ -504,15 +506,15 @@ __device__ void wl_compact_blk(int n, Pred pred, int* list, int* cnt) {
         int off = bbase + (wib ? wsum[wib - 1] : 0) + x - c;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (bits >> q & 1u) list[off++] = k0 + q;
+            if (bits >> q & 1u) list[off++] = vals[q];
         __syncthreads();
     }
 }
 __device__ void wl_compact(const int* mark, int stamp, int n, int* list, int* cnt, int, int) {
-    wl_compact_blk(n, [&](int k) { return mark[k] == stamp; }, list, cnt);
+    wl_compact_blk(n, [&](int k, int& v) { v = k; return mark[k] == stamp; }, list, cnt);
 }
 __device__ void wl_compact_st(const uint8_t* st, int n, int* list, int* cnt, int, int) {
-    wl_compact_blk(n, [&](int k) { return st[k] == 0; }, list, cnt);
+    wl_compact_blk(n, [&](int k, int& v) { v = k; return st[k] == 0; }, list, cnt);
 }
 
 // rows longer than kLongRow, appended in any order
@@ -710,30 +712,31 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             if (!any) break;
         }
         // commit: admitted vertices and centers are processed, seeded by
-        // owner; the rest form the next pass's U (compacted in vertex order)
-        int left = 0;
+        // owner; the rest of U is appended to the next pass's U in the same
+        // sweep (block-tiled, so pass 0 keeps vertex order within a tile)
         int* ucnt = (int*)&ctl[11 + ps];
-        for (int t = tid; t < U.cnt; t += nth) {
-            const int j = U[t];
-            const uint8_t sj = g.st[j];
-            if (sj == 1 || (sj == 0 && adm[j])) { g.seed_of[j] = g.owner[j]; g.st[j] = 2; }
-            else if (sj == 0) ++left;
-        }
-        left = __reduce_add_sync(0xffffffffu, left);
-        if (lane == 0 && left) atomicAdd((int*)&ctl[3 + ps], left);
+        wl_compact_blk(
+            U.cnt,
+            [&](int t, int& v) {
+                const int j = U[t];
+                v = j;
+                const uint8_t sj = g.st[j];
+                if (sj == 1 || (sj == 0 && adm[j])) {
+                    g.seed_of[j] = g.owner[j];
+                    g.st[j] = 2;
+                    return false;
+                }
+                return sj == 0;
+            },
+            unext, ucnt);
         grid.sync();
         AGG_STAMP(7);
-        if (ctl[3 + ps] > 0) {
-            wl_compact_st(g.st, n, unext, ucnt, tid, nth);
-            grid.sync();
-            AGG_STAMP(8);
-        }
         if (g.prof && tid == 0 && pass < 32) {
             g.prof[4 * pass + 2] = H.cnt;
             g.prof[4 * pass + 3] = itg - itg0;
         }
-        remaining = ctl[3 + ps];
-        U = WL{unext, ctl[11 + ps]};
+        remaining = ctl[11 + ps];
+        U = WL{unext, remaining};
         if (ctl[ps] == 0) { ++pass; break; }  // no centers (cannot happen, U/aggregation.py:190)
     }
     if (tid == 0) { ctl[9] = pass; ctl[10] = remaining; }
