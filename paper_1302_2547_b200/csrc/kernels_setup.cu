@@ -395,6 +395,71 @@ struct WL {
     __device__ __forceinline__ int operator[](int t) const { return list ? list[t] : t; }
 };
 
+// Long rows (> kLongRow entries) of a phase: `team` warps of one CTA per row
+// (team = the power of two that spreads the level's long rows over the whole
+// grid, up to the CTA), so a hub row of thousands of entries is not one
+// warp's serial chain of dependent gathers.  filt(k): whether row k takes
+// part (evaluated identically by every warp of its team); part(k, e, e1,
+// step, bs, bi): key maximum over entries e, e + step, ... < e1; fin(k, bs,
+// bi): the row's result, called by one thread.  The key order is total, so
+// the split does not change any maximum.  Iterations are CTA-uniform, so
+// __syncthreads joins a team's warps.
+__device__ __forceinline__ int long_team(int nlong, int nw) {
+    const int W = blockDim.x >> 5;
+    if (nlong <= 0) return 1;
+    int t = 1;
+    while (2 * t <= W && 2 * t * nlong <= nw) t *= 2;
+    return t;
+}
+template <class Filt, class Part, class Fin>
+__device__ __forceinline__ void agg_long(const AggCoop& g, int nlong, int team, int lane, int w, int nw, Filt filt,
+                                         Part part, Fin fin) {
+    const Csr& A = g.A;
+    if (team <= 1) {
+        for (int t = w; t < nlong; t += nw) {
+            const int k = g.longs[t];
+            if (!filt(k)) continue;
+            double bs = 0.0;
+            int bi = -1;
+            part(k, A.rp[k] + lane, A.rp[k + 1], 32, bs, bi);
+            warp_keymax(bs, bi);
+            if (lane == 0) fin(k, bs, bi);
+        }
+        return;
+    }
+    __shared__ double tbs[32];
+    __shared__ int tbi[32];
+    const int wib = threadIdx.x >> 5, tpb = (blockDim.x >> 5) / team;
+    for (int base = blockIdx.x * tpb; base < nlong; base += gridDim.x * tpb) {
+        const int li = base + wib / team;
+        double bs = 0.0;
+        int bi = -1;
+        int k = -1;
+        if (li < nlong) {
+            k = g.longs[li];
+            if (filt(k))
+                part(k, A.rp[k] + (wib % team) * 32 + lane, A.rp[k + 1], 32 * team, bs, bi);
+            else
+                k = -1;
+        }
+        warp_keymax(bs, bi);
+        if (lane == 0) {
+            tbs[wib] = bs;
+            tbi[wib] = bi;
+        }
+        __syncthreads();
+        if (k >= 0 && wib % team == 0 && lane == 0) {
+            for (int q = 1; q < team; ++q) {
+                const double s2 = tbs[wib + q];
+                const int i2 = tbi[wib + q];
+                if (i2 >= 0 && (bi < 0 || key_gt(s2, i2, bs, bi))) { bs = s2; bi = i2; }
+            }
+            fin(k, bs, bi);
+        }
+        __syncthreads();
+    }
+}
+
 // hop1 over the items of H: max key over the row's unprocessed (mode 0) or
 // center (mode 1) neighbours
 __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int stamp, int nlong, int tid, int nth, int lane, int w,
@@ -426,45 +491,33 @@ __device__ void coop_hop1(const AggCoop& g, WL H, int mode, int stamp, int nlong
         g.ms[k] = bs;
         g.mi[k] = bi;
     }
-    for (int t = w; t < nlong; t += nw) {
-        const int k = g.longs[t];
-        if (H.list && g.mark[k] != stamp) continue;  // not in H
-        const int e0 = A.rp[k], e1 = A.rp[k + 1];
-        double bs = 0.0;
-        int bi = -1;
-        for (int e = e0 + lane; e < e1; e += 128) {
-            int j[4];
-            uint8_t sj[4];
-            double v[4];
+    agg_long(
+        g, nlong, long_team(nlong, nw), lane, w, nw, [&](int k) { return !H.list || g.mark[k] == stamp; },
+        [&](int, int e, int e1, int step, double& bs, int& bi) {
+            for (; e < e1; e += 4 * step) {
+                int j[4];
+                uint8_t sj[4];
+                double v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) j[q] = e + 32 * q < e1 ? __ldg(A.ci + e + 32 * q) : -1;
+                for (int q = 0; q < 4; ++q) j[q] = e + step * q < e1 ? __ldg(A.ci + e + step * q) : -1;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                sj[q] = j[q] >= 0 ? g.st[j[q]] : (mode == 0 ? 2 : 0);  // padding: skipped
-                v[q] = j[q] >= 0 ? g.sc[j[q]] : 0.0;
+                for (int q = 0; q < 4; ++q) {
+                    sj[q] = j[q] >= 0 ? g.st[j[q]] : (mode == 0 ? 2 : 0);  // padding: skipped
+                    v[q] = j[q] >= 0 ? g.sc[j[q]] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (mode == 0 ? (sj[q] == 2) : (sj[q] != 1)) continue;
+                    if (bi < 0 || key_gt(v[q], j[q], bs, bi)) { bs = v[q]; bi = j[q]; }
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (mode == 0 ? (sj[q] == 2) : (sj[q] != 1)) continue;
-                if (bi < 0 || key_gt(v[q], j[q], bs, bi)) { bs = v[q]; bi = j[q]; }
-            }
-        }
-        warp_keymax(bs, bi);
-        if (lane == 0) { g.ms[k] = bs; g.mi[k] = bi; }
-    }
+        },
+        [&](int k, double bs, int bi) {
+            g.ms[k] = bs;
+            g.mi[k] = bi;
+        });
 }
 
-// append every k in [0, n) with flag[k] == stamp to list, in vertex order
-// within each warp (one atomic per warp)
-__device__ __forceinline__ void wl_append(bool f, int k, int* list, int* cnt) {
-    const unsigned m = __ballot_sync(0xffffffffu, f);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
-    int b = 0;
-    if (lane == 0) b = atomicAdd(cnt, __popc(m));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (f) list[b + __popc(m & ((1u << lane) - 1u))] = k;
-}
 // block-aggregated compaction: each thread tests 4 consecutive vertices, a
 // block scan places them and ONE atomic per block tile reserves the range
 // (one atomic per warp was ~65K same-address atomics at level 0, ~45 us)
@@ -610,16 +663,15 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             row_hopmax(A, g.ms, g.mi, i, e0, e1, 1, bs, bi);
             if (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi)) { g.st[i] = 1; ++local; }
         }
-        for (int t = w; t < nlong; t += nw) {
-            const int i = g.longs[t];
-            if (g.st[i] != 0) continue;  // in U and not yet a center
-            const int e0 = A.rp[i], e1 = A.rp[i + 1];
-            double bs = 0.0;
-            int bi = -1;
-            row_hopmax(A, g.ms, g.mi, i, e0 + lane, e1, 32, bs, bi);
-            warp_keymax(bs, bi);
-            if (lane == 0 && (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi))) { g.st[i] = 1; ++local; }
-        }
+        const int team = long_team(nlong, nw);
+        auto hopmax = [&](int k, int e, int e1, int step, double& bs, int& bi) {
+            row_hopmax(A, g.ms, g.mi, k, e, e1, step, bs, bi);
+        };
+        agg_long(
+            g, nlong, team, lane, w, nw, [&](int i) { return g.st[i] == 0; }, hopmax,  // in U, not yet a center
+            [&](int i, double bs, int bi) {
+                if (bi < 0 || bi == i || key_gt(g.sc[i], i, bs, bi)) { g.st[i] = 1; ++local; }
+            });
         // one atomic per warp: per-thread same-address atomics serialise in L2
         // (~300K of them at level 0 cost ~100 us per phase)
         local = __reduce_add_sync(0xffffffffu, local);
@@ -643,16 +695,9 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
             row_hopmax(A, g.ms, g.mi, j, e0, e1, 1, bs, bi);
             g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
         }
-        for (int t = w; t < nlong; t += nw) {
-            const int j = g.longs[t];
-            if (g.st[j] != 0) continue;
-            const int e0 = A.rp[j], e1 = A.rp[j + 1];
-            double bs = 0.0;
-            int bi = -1;
-            row_hopmax(A, g.ms, g.mi, j, e0 + lane, e1, 32, bs, bi);
-            warp_keymax(bs, bi);
-            if (lane == 0) g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1;
-        }
+        agg_long(
+            g, nlong, team, lane, w, nw, [&](int j) { return g.st[j] == 0; }, hopmax,
+            [&](int j, double bs, int bi) { g.owner[j] = (bi >= 0 && !(bs < g.sc[j])) ? bi : -1; });
         grid.sync();
         AGG_STAMP(5);
         // admission fixpoint (uncapped sweeps of K/numba_backend.py:235-273)
@@ -684,26 +729,31 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
                 }
                 if (f) { adm[j] = 1; ch = 1; }
             }
-            for (int t = w; t < nlong; t += nw) {
-                const int j = g.longs[t];
-                if (g.st[j] == 2) continue;  // processed: not in U
-                const int c = g.owner[j];
-                const int e0 = A.rp[j], e1 = A.rp[j + 1];
-                if (c < 0 || c == j || adm[j]) continue;
-                bool f = false;
-                for (int e = e0 + lane; e < e1 && !f; e += 128) {
-                    int nb[4];
+            agg_long(
+                g, nlong, team, lane, w, nw,
+                [&](int j) {  // in U, claimed by another center, not yet admitted
+                    const int c = g.owner[j];
+                    return g.st[j] != 2 && c >= 0 && c != j && !adm[j];
+                },
+                [&](int j, int e, int e1, int step, double& bs, int& bi) {
+                    const int c = g.owner[j];
+                    bool f = false;
+                    for (; e < e1 && !f; e += 4 * step) {
+                        int nb[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) nb[q] = e + 32 * q < e1 ? __ldg(A.ci + e + 32 * q) : j;  // j: not admitted
-                    uint8_t av[4];
-                    int ov[4];
+                        for (int q = 0; q < 4; ++q) nb[q] = e + step * q < e1 ? __ldg(A.ci + e + step * q) : j;
+                        uint8_t av[4];
+                        int ov[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) { av[q] = adm[nb[q]]; ov[q] = g.owner[nb[q]]; }
+                        for (int q = 0; q < 4; ++q) { av[q] = adm[nb[q]]; ov[q] = g.owner[nb[q]]; }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) f |= av[q] && ov[q] == c;
-                }
-                if (__any_sync(0xffffffffu, f) && lane == 0) { adm[j] = 1; ch = 1; }
-            }
+                        for (int q = 0; q < 4; ++q) f |= av[q] && ov[q] == c;
+                    }
+                    if (f) { bs = 0.0; bi = 0; }  // found: any key
+                },
+                [&](int j, double, int bi) {
+                    if (bi >= 0) { adm[j] = 1; ch = 1; }
+                });
             if (__any_sync(0xffffffffu, ch) && lane == 0) atomicOr((int*)&ctl[6 + slot], 1);
             grid.sync();
             AGG_STAMP(6);
