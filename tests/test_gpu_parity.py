@@ -197,6 +197,56 @@ def test_random_graphs_vs_oracle(U, oracle, seed, cap, ppl):
     assert err.max() <= 1e-9
 
 
+@pytest.mark.parametrize("seed,weights,nhub,n", [(1, "int", 4, 4000), (2, "bigint", 4, 4000), (3, "float", 4, 4000),
+                                                 (4, "bigint", 0, 4000), (5, "int", 12, 40000)])
+def test_hub_graphs_vs_oracle(U, oracle, seed, weights, nhub, n):
+    """Graphs with hub vertices (rows of 100-400 entries) checked live
+    against the CPU oracle: the long-row team paths of the aggregation, the
+    chunked global-table Galerkin (integer weights), the int64 shared-table
+    Galerkin (weights ~2^24, no hubs) and the reference-ordered float path."""
+    rng = np.random.default_rng(seed)
+    from scipy.spatial import cKDTree
+    Pt = rng.random((n, 2))
+    pairs = cKDTree(Pt).query_pairs(np.sqrt(8.0 / (np.pi * n)), output_type="ndarray")
+    hubs = rng.choice(n, nhub, replace=False)
+    extra = [np.stack([np.full(k, h), rng.choice(n, k, replace=False)], 1)
+             for h, k in zip(hubs, rng.integers(100, 400, hubs.size))]
+    pairs = np.concatenate([pairs] + extra)
+    pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+    pairs = np.unique(np.sort(pairs, 1), axis=0)
+    if weights == "int":
+        w = rng.integers(1, 4, pairs.shape[0]).astype(np.float64)
+    elif weights == "bigint":
+        w = rng.integers(1 << 23, 1 << 24, pairs.shape[0]).astype(np.float64)
+    else:
+        w = rng.uniform(0.1, 3.0, pairs.shape[0])
+    rows = np.concatenate([pairs[:, 0], pairs[:, 1]])
+    cols = np.concatenate([pairs[:, 1], pairs[:, 0]])
+    vals = np.concatenate([-w, -w])
+    deg = np.bincount(rows, weights=w[np.r_[np.arange(w.size), np.arange(w.size)]], minlength=n)
+    diag = (deg + 1.0 if weights == "int" else np.floor(deg * 1.0625) + 1.0 if weights == "bigint"
+            else deg + rng.uniform(0.05, 0.5, n))
+    A = U.SparseMatrix.from_coo(n, n, np.r_[rows, np.arange(n)], np.r_[cols, np.arange(n)], np.r_[vals, diag])
+    assert nhub == 0 or np.diff(A.indptr).max() > 64
+    ho = oracle.setup(A.indptr, A.indices, A.data, seed=seed)
+    hg = U.setup(A, U.AggregationConfig(seed=seed))
+    assert hg.n_levels == ho.n_levels
+    for Lg, Lo in zip(hg.levels, ho.levels):
+        m = Lg.matrix
+        assert np.array_equal(m.indptr, Lo.indptr) and np.array_equal(m.indices, Lo.indices)
+        assert np.array_equal(m.data, Lo.data)
+        if Lo.vertex_to_agg is not None:
+            assert np.array_equal(Lg.aggregation.vertex_to_agg, Lo.vertex_to_agg)
+    b = rng.standard_normal(n)
+    xo, ro = oracle.npcg_solve(ho, b, tol=1e-10, max_iters=300)
+    xg, rg = U.npcg_solve(hg, U.CycleSpec(), U.Smoother(), b, tol=1e-10, max_iters=300)
+    assert abs(rg.iterations - ro.iterations) <= 1
+    m = min(len(rg.residual_history), len(ro.residual_history))
+    h1, h2 = np.array(rg.residual_history[:m]), np.array(ro.residual_history[:m])
+    err = np.where(np.abs(h1 - h2) <= 1e-13, 0, np.abs(h1 - h2) / h2)
+    assert err.max() <= 1e-9
+
+
 def test_edge_cases(U):
     from paper_1302_2547_b200 import problems as P
     # n0 >= n: single level, direct solve
