@@ -64,21 +64,23 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // Generation barrier over a co-resident (cooperatively launched) grid:
 // bar[0] arrivals (back to 0 after each barrier), bar[1] generation.
 __device__ __noinline__ inline void coop_grid_sync(unsigned* bar) {
+    // bar: a 64-bit arrival counter, zeroed once and only ever used by
+    // launches of one grid size, so it is a multiple of gridDim.x at every
+    // launch start.  Arrive with release, spin with acquire until this
+    // epoch's gridDim.x arrivals are in: no last-arriver round trip, no full
+    // fences (the acquire invalidates L1 for the CTA's later plain loads).
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            const long long t0 = clock64();
-            while (*gen == g)
-                if (clock64() - t0 > (1ll << 34)) __trap();  // a lost CTA: fail loudly
+        unsigned long long* c = reinterpret_cast<unsigned long long*>(bar);
+        unsigned long long old, v;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(c) : "memory");
+        const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+        const long long t0 = clock64();
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+            if (v >= target) break;
+            if (clock64() - t0 > (1ll << 34)) __trap();  // a lost CTA: fail loudly
         }
-        __threadfence();
     }
     __syncthreads();
 }

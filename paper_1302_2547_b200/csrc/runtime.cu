@@ -346,8 +346,8 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         UA_CK(cudaStreamSynchronize(s));  // host vector is a temporary
     }
     ws->fpart.alloc(2 * (size_t)kNumSMs * 8, s);
-    ws->fbar.alloc(2, s);
-    UA_CK(cudaMemsetAsync(ws->fbar.p, 0, 2 * sizeof(unsigned), s));
+    ws->fbar.alloc(2 * (size_t)nl, s);  // one 64-bit arrival counter per level (fixed grid per level)
+    UA_CK(cudaMemsetAsync(ws->fbar.p, 0, 2 * (size_t)nl * sizeof(unsigned), s));
     const bool sing = h->singular;
     if (wsprof) {
         UA_CK(cudaStreamSynchronize(s));
