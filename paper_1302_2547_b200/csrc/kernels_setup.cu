@@ -1099,24 +1099,37 @@ __global__ void __launch_bounds__(32 * kGalWarps) k_galerkin_int_warp(Csr A, int
             }
         }
         __syncwarp();
+        // drop exact zeros (K/numba_backend.py:164) compacting the kept
+        // entries in place to the front of the table, then write each at its
+        // rank among the row's keys: the row leaves here sorted by coarse
+        // column, so no segmented sort is needed afterwards
         int c = 0;
-        const size_t o = (size_t)soff[I];
         for (int t0 = 0; t0 < cap; t0 += 32) {
             const int t = t0 + lane;
             int key = -1;
-            double v = 0.0;
+            T v = 0;
             if (t < cap) {
                 key = K[t];
-                v = (double)V[t];
+                v = V[t];
             }
-            const bool keep = key >= 0 && v != 0.0;
+            const bool keep = key >= 0 && v != 0;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();  // the round's reads precede its writes (positions <= t)
             if (keep) {
                 const int pos = c + __popc(bal & ((1u << lane) - 1u));
-                tk[o + pos] = key;
-                tv[o + pos] = v;
+                K[pos] = key;
+                V[pos] = v;
             }
             c += __popc(bal);
+            __syncwarp();
+        }
+        const size_t o = (size_t)soff[I];
+        for (int t = lane; t < c; t += 32) {
+            const int key = K[t];
+            int rank = 0;
+            for (int u = 0; u < c; ++u) rank += K[u] < key;  // broadcast reads
+            tk[o + rank] = key;
+            tv[o + rank] = (double)V[t];
         }
         if (lane == 0) cnt[I] = c;
         __syncwarp();
@@ -1671,20 +1684,23 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     ci_c.alloc(std::max(nnz_c, 1), s);
     av_c.alloc(std::max(nnz_c, 1), s);
     if (nnz_c > 0) {
-        DBuf<int> ck(nnz_c, s);
-        DBuf<double> cv(nnz_c, s);
-        if (warp_path)
+        if (warp_path) {
+            // rows already sorted by the warp kernel: place them straight
+            // into the output CSR
             UA_LAUNCH(k_galerkin_place, std::min(cdiv(nc, 8), 148 * 16), 256, 0, s, nc, soff.p, cnt.p, rp_c.p, tk.p,
-                      tv.p, ck.p, cv.p);
-        else
+                      tv.p, ci_c.p, av_c.p);
+        } else {
+            DBuf<int> ck(nnz_c, s);
+            DBuf<double> cv(nnz_c, s);
             UA_LAUNCH(k_galerkin_compact, cdiv(nc, 8), 256, 0, s, nc, soff.p, slen.p, hkey.p, hval.p, rp_c.p, ck.p,
                       cv.p);
-        size_t tmp = 0;
-        UA_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
-                                                  rp_c.p + 1, s));
-        DBuf<char> t(tmp, s);
-        UA_CK(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
-                                                  rp_c.p + 1, s));
+            size_t tmp = 0;
+            UA_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
+                                                      rp_c.p + 1, s));
+            DBuf<char> t(tmp, s);
+            UA_CK(cub::DeviceSegmentedSort::SortPairs(t.p, tmp, ck.p, ci_c.p, cv.p, av_c.p, nnz_c, nc, rp_c.p,
+                                                      rp_c.p + 1, s));
+        }
     }
     gt("sort");
     return nnz_c;
