@@ -756,6 +756,16 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
                     for (int q = 0; q < 8; ++q) { av[q] = adm[nb[q]]; ov[q] = g.owner[nb[q]]; }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) f |= av[q] && ov[q] == c;
+                    // j is admitted: so is every same-owner neighbour already
+                    // loaded (the fixpoint is reachability from the center
+                    // through same-owner vertices, so admitting them now only
+                    // shortens the sweep chain; owner == a current center
+                    // implies the vertex is in U)
+                    if (f) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (!av[q] && ov[q] == c && nb[q] != c && nb[q] != j) adm[nb[q]] = 1;
+                    }
                 }
                 if (f) { adm[j] = 1; ch = 1; }
             }
