@@ -67,8 +67,9 @@ __device__ __noinline__ inline void coop_grid_sync(unsigned* bar) {
     // bar: a 64-bit arrival counter, zeroed once and only ever used by
     // launches of one grid size, so it is a multiple of gridDim.x at every
     // launch start.  Arrive with release, spin with acquire until this
-    // epoch's gridDim.x arrivals are in: no last-arriver round trip, no full
-    // fences (the acquire invalidates L1 for the CTA's later plain loads).
+    // epoch's gridDim.x arrivals are in (relaxed polling: an acquire per poll
+    // would invalidate the SM's L1 under its co-resident CTAs), then one
+    // acquire fence (which invalidates L1 for the CTA's later plain loads).
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long* c = reinterpret_cast<unsigned long long*>(bar);
@@ -77,10 +78,11 @@ __device__ __noinline__ inline void coop_grid_sync(unsigned* bar) {
         const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
         const long long t0 = clock64();
         while (true) {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
             if (v >= target) break;
             if (clock64() - t0 > (1ll << 34)) __trap();  // a lost CTA: fail loudly
         }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire once, after the relaxed spin
     }
     __syncthreads();
 }

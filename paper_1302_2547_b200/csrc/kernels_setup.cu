@@ -581,9 +581,10 @@ __global__ void k_long_rows(Csr A, int* list, int* cnt) {
 // scope; the acquire invalidates L1, so plain loads see the other CTAs'
 // global writes)
 // Grid barrier on a monotonic arrival counter (ctl[20], zeroed per launch):
-// thread 0 of each CTA adds with release semantics and spins with acquire
-// loads until every CTA of this epoch has arrived (the acquire also
-// invalidates L1, so plain loads after the barrier see other CTAs' writes).
+// thread 0 of each CTA adds with release semantics, spins with relaxed loads
+// until every CTA of this epoch has arrived, then fences once (acquire; it
+// also invalidates L1, so plain loads after the barrier see other CTAs'
+// writes).
 // No last-arriver round trip and no full fences: ~1 us cheaper per phase
 // than cg::grid_group::sync().  A lost CTA traps instead of hanging.
 struct GridBar {
@@ -599,10 +600,11 @@ struct GridBar {
             const long long t0 = clock64();
             unsigned v;
             while (true) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
                 if ((int)(v - target) >= 0) break;
                 if (clock64() - t0 > (1ll << 34)) __trap();
             }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // one acquire after the relaxed spin
         }
         __syncthreads();
     }
