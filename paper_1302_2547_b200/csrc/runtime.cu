@@ -52,22 +52,72 @@ __global__ void k_compose_seeds(int nc2, const int* seeds1, const int* sb, int* 
 
 static int g1d(long long n) { return std::max(1, std::min(cdiv(n, 256), 4 * kNumSMs)); }
 
-// U/hierarchy.py:112-117
-static bool detect_singular(const Level& L, cudaStream_t s) {
-    if (L.nnz == 0) return true;
-    DBuf<double> ones(L.n, s), y(L.n, s);
+// U/hierarchy.py:112-117: singular iff max|A·1| <= 1e-10 max|a|.  One pass
+// over the values: A·1 row sums (products by 1.0 are exact, so each row sum
+// is the SpMV's sequential sum bit for bit) and max|a| together; the
+// result is copied to pinned memory and read only when the coarsest level
+// needs it, so setup does not stop here for a host round trip.
+__global__ void k_singular_check(Csr A, unsigned long long* out) {
+    double ma = 0.0, mr = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+        double r = 0.0;
+        for (int e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            const double a = __ldg(A.av + e);
+            r = __dadd_rn(r, a);
+            ma = fmax(ma, fabs(a));
+        }
+        mr = fmax(mr, fabs(r));
+    }
+    ma = block_max(ma);
+    mr = block_max(mr);
+    if (threadIdx.x == 0) {
+        atomicMax(out, (unsigned long long)__double_as_longlong(ma));
+        atomicMax(out + 1, (unsigned long long)__double_as_longlong(mr));
+    }
+}
+struct SingularCheck {
+    unsigned long long* h = nullptr;  // pinned {max|a|, max|A·1|}
+    cudaEvent_t ev = nullptr;
+    bool trivial = false;             // no entries: singular
+    SingularCheck() = default;
+    SingularCheck(const SingularCheck&) = delete;
+    SingularCheck& operator=(const SingularCheck&) = delete;
+    SingularCheck(SingularCheck&& o) noexcept : h(o.h), ev(o.ev), trivial(o.trivial) { o.ev = nullptr; }
+    SingularCheck& operator=(SingularCheck&& o) noexcept {
+        std::swap(h, o.h);
+        std::swap(ev, o.ev);
+        std::swap(trivial, o.trivial);
+        return *this;
+    }
+    ~SingularCheck() {
+        if (ev) cudaEventDestroy(ev);  // setup left early (error path)
+    }
+};
+static SingularCheck singular_launch(const Level& L, cudaStream_t s) {
+    SingularCheck c;
+    if (L.nnz == 0) {
+        c.trivial = true;
+        return c;
+    }
+    static thread_local unsigned long long* hp = nullptr;
+    if (!hp) UA_CK(cudaMallocHost(&hp, 2 * sizeof(unsigned long long)));
     DBuf<unsigned long long> mx(2, s);
     UA_CK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
-    UA_LAUNCH(k_fill, g1d(L.n), 256, 0, s, L.n, ones.p, 1.0);
-    launch_spmv(L.csr(), L.groups(), ones.p, y.p, s);
-    UA_LAUNCH(k_maxabs_vals, g1d(L.nnz), 256, 0, s, (int)L.nnz, L.av.p, mx.p);
-    UA_LAUNCH(k_maxabs_vals, g1d(L.n), 256, 0, s, L.n, y.p, mx.p + 1);
-    unsigned long long h[2];
-    UA_CK(cudaMemcpyAsync(h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    UA_CK(cudaStreamSynchronize(s));
+    UA_LAUNCH(k_singular_check, g1d(L.n), 256, 0, s, L.csr(), mx.p);
+    UA_CK(cudaMemcpyAsync(hp, mx.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
+    UA_CK(cudaEventRecord(c.ev, s));
+    c.h = hp;
+    return c;
+}
+static bool singular_result(SingularCheck& c) {
+    if (c.trivial) return true;
+    UA_CK(cudaEventSynchronize(c.ev));
+    cudaEventDestroy(c.ev);
+    c.ev = nullptr;
     double scale, ax;
-    std::memcpy(&scale, &h[0], 8);
-    std::memcpy(&ax, &h[1], 8);
+    std::memcpy(&scale, &c.h[0], 8);
+    std::memcpy(&ax, &c.h[1], 8);
     return ax <= 1e-10 * scale;
 }
 
@@ -202,7 +252,9 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     mark("copy");
     finish_level(*L0, s);
     mark("groups0");
-    h->singular = P.singular < 0 ? detect_singular(*L0, s) : (P.singular != 0);
+    SingularCheck scheck;
+    if (P.singular < 0) scheck = singular_launch(*L0, s);
+    else h->singular = (P.singular != 0);
     mark("singular");
     const int max_levels = P.max_levels;
     std::unique_ptr<Level> cur = std::move(L0);
@@ -229,6 +281,7 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         cur = std::move(nxt);
     }
     h->levels.push_back(std::move(cur));
+    if (P.singular < 0) h->singular = singular_result(scheck);
     h->coarse_mode = device_coarse_factor(h->levels.back()->csr(), h->singular, h->Minv, s);
     mark("coarse");
     UA_CK(cudaEventRecord(e1, s));
