@@ -1595,25 +1595,6 @@ void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cu
     UA_LAUNCH(k_seg_starts, grid_for(n), 256, 0, s, n, nc, keys_out.p, agg_ptr);
 }
 
-// true when every value is an integer and nnz * max|a| < 2^52 (exact in any order)
-static bool integer_exact(const Csr& A, cudaStream_t s, double* maxabs = nullptr) {
-    if (maxabs) *maxabs = 0.0;
-    if (A.nnz == 0) return true;
-    DBuf<int> bad(1, s);
-    DBuf<unsigned long long> mx(1, s);
-    UA_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-    UA_CK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
-    UA_LAUNCH(k_int_check, grid_for(A.nnz), 256, 0, s, (long long)A.nnz, A.av, bad.p, mx.p);
-    int h_bad = 0;
-    unsigned long long h_mx = 0;
-    UA_CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    UA_CK(cudaMemcpyAsync(&h_mx, mx.p, sizeof(h_mx), cudaMemcpyDeviceToHost, s));
-    UA_CK(cudaStreamSynchronize(s));
-    double m;
-    std::memcpy(&m, &h_mx, 8);
-    if (maxabs) *maxabs = m;
-    return h_bad == 0 && (double)A.nnz * m < 4503599627370496.0;  // 2^52
-}
 
 // Galerkin: returns nnz_c; allocates out arrays
 long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
@@ -1637,27 +1618,37 @@ long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_p
     const size_t hsz = 2 * (size_t)std::max(A.nnz, 1);
     SPtr<int> hkey{scratch<int>(0, hsz)};
     SPtr<double> hval{scratch<double>(1, hsz)};
+    // integrality / magnitude of A and the longest aggregate stream, read
+    // back together (one host round trip chooses the path)
+    bool exact_int = true, warp_path = false;
     double maxabs = 0.0;
-    const bool exact_int = integer_exact(A, s, &maxabs);
+    if (A.nnz > 0) {
+        DBuf<int> bad(1, s), smx(1, s);
+        DBuf<unsigned long long> amx(1, s);
+        UA_CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        UA_CK(cudaMemsetAsync(amx.p, 0, sizeof(unsigned long long), s));
+        UA_LAUNCH(k_int_check, grid_for(A.nnz), 256, 0, s, (long long)A.nnz, A.av, bad.p, amx.p);
+        size_t tmp = 0;
+        UA_CK(cub::DeviceReduce::Max(nullptr, tmp, slen.p, smx.p, nc, s));
+        DBuf<char> t(tmp, s);
+        UA_CK(cub::DeviceReduce::Max(t.p, tmp, slen.p, smx.p, nc, s));
+        int h_bad = 0, h_smx = 0;
+        unsigned long long h_amx = 0;
+        UA_CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaMemcpyAsync(&h_amx, amx.p, sizeof(h_amx), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaMemcpyAsync(&h_smx, smx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        std::memcpy(&maxabs, &h_amx, 8);
+        exact_int = h_bad == 0 && (double)A.nnz * maxabs < 4503599627370496.0;  // 2^52
+        // warp-per-aggregate shared-memory tables when every aggregate's
+        // stream is short (fine levels); otherwise (hub aggregates of coarse
+        // levels) the all-threads global table, whose parallelism does not
+        // depend on the longest stream
+        warp_path = exact_int && h_smx <= kGalStreamMax;
+    }
     gt("intcheck");
     SPtr<int> tk{nullptr};
     SPtr<double> tv{nullptr};
-    // warp-per-aggregate shared-memory tables when every aggregate's stream
-    // is short (fine levels); otherwise (hub aggregates of coarse levels) the
-    // all-threads global table, whose parallelism does not depend on the
-    // longest stream
-    bool warp_path = false;
-    if (exact_int) {
-        DBuf<int> mx(1, s);
-        size_t tmp = 0;
-        UA_CK(cub::DeviceReduce::Max(nullptr, tmp, slen.p, mx.p, nc, s));
-        DBuf<char> t(tmp, s);
-        UA_CK(cub::DeviceReduce::Max(t.p, tmp, slen.p, mx.p, nc, s));
-        int h_mx = 0;
-        UA_CK(cudaMemcpyAsync(&h_mx, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        UA_CK(cudaStreamSynchronize(s));
-        warp_path = h_mx <= kGalStreamMax;
-    }
     if (exact_int && !warp_path) {
         UA_CK(cudaMemsetAsync(hkey.p, 0xff, sizeof(int) * hsz, s));
         UA_CK(cudaMemsetAsync(hval.p, 0, sizeof(double) * hsz, s));
