@@ -282,9 +282,15 @@ def run_ours(args, rank, ws, local):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    diag = {"host_setup": [], "host_solve": [], "dev_solve": []}  # per-step diagnostics
+
     def step(profile=False):
+        t0 = time.perf_counter()
         h = U.setup(Ad)
+        t1 = time.perf_counter()
         x, rep = solve(h, profile)
+        diag["host_setup"].append(t1 - t0)
+        diag["host_solve"].append(time.perf_counter() - t1)
         return h, x, rep
 
     def solve(h, profile):
@@ -298,6 +304,7 @@ def run_ours(args, rank, ws, local):
         _lib.check(_lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), b.data_ptr(), None, x.data_ptr(),
                                                 hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res),
                                                 stream.cuda_stream))
+        diag["dev_solve"].append(res.solve_seconds)
         return x, (res.iterations, hist[: res.iterations + 1])
 
     def barrier():
@@ -321,6 +328,7 @@ def run_ours(args, rank, ws, local):
     # the measured interval.  Every step still does all of its work.
     gc.collect()
     gc.disable()
+    d0 = len(diag["dev_solve"])
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.zero_()
@@ -432,6 +440,7 @@ def run_ours(args, rank, ws, local):
                    "solve_s": t_step - float(np.mean(setup_s)),
                    "l2": "flushed between steps (256 MB write, outside the step events); matrix 175 MB > L2",
                    "python_gc": "collected before, paused during the timed steps",
+                   "step_diag": {k: [round(float(v), 5) for v in diag[k][d0:d0 + args.steps]] for k in diag},
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "true_relres": relres, "level0_kernels": kern,
                    "level0_kernels_c5_slab": slab},

@@ -203,7 +203,9 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         static size_t reserved = 0;
         const size_t want = (size_t)40 * (size_t)nnz + (size_t)64 * (size_t)n;
         size_t fr = 0, tot = 0;
-        UA_CK(cudaMemGetInfo(&fr, &tot));
+        // (cudaMemGetInfo only when the pool would grow: it is a driver query
+        // that can stall behind outstanding frees)
+        if (want > reserved) UA_CK(cudaMemGetInfo(&fr, &tot));
         if (want > reserved && want < fr / 2) {
             void* p = nullptr;
             UA_CK(cudaMallocAsync(&p, want, s));
