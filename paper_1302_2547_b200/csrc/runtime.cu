@@ -333,21 +333,33 @@ constexpr int kFlagSlots = 1024, kFlagStride = 4;
 // exec is much cheaper than a fresh instantiation).
 namespace {
 std::mutex g_graph_mu;
-std::vector<cudaGraphExec_t> g_graph_cache;
-constexpr size_t kGraphCacheMax = 4;
+struct CachedGraph {
+    cudaGraphExec_t e;
+    int par;
+    size_t nodes;
+};
+std::vector<CachedGraph> g_graph_cache;
+constexpr size_t kGraphCacheMax = 8;
 }  // namespace
-cudaGraphExec_t graph_cache_take() {
+cudaGraphExec_t graph_cache_take(int par, size_t nodes) {
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    if (g_graph_cache.empty()) return nullptr;
-    cudaGraphExec_t e = g_graph_cache.back();
-    g_graph_cache.pop_back();
-    return e;
+    for (size_t k = g_graph_cache.size(); k-- > 0;) {
+        if (g_graph_cache[k].par == par && g_graph_cache[k].nodes == nodes) {
+            cudaGraphExec_t e = g_graph_cache[k].e;
+            g_graph_cache.erase(g_graph_cache.begin() + k);
+            return e;
+        }
+    }
+    return nullptr;
 }
-void graph_cache_give(cudaGraphExec_t e) {
+void graph_cache_give(cudaGraphExec_t e, int par, size_t nodes) {
     if (!e) return;
     std::lock_guard<std::mutex> lk(g_graph_mu);
-    if (g_graph_cache.size() < kGraphCacheMax) g_graph_cache.push_back(e);
-    else cudaGraphExecDestroy(e);
+    if (g_graph_cache.size() >= kGraphCacheMax) {  // evict the oldest
+        cudaGraphExecDestroy(g_graph_cache.front().e);
+        g_graph_cache.erase(g_graph_cache.begin());
+    }
+    g_graph_cache.push_back({e, par, nodes});
 }
 
 int mapped_slot_acquire(int** host, int** dev) {
@@ -567,7 +579,10 @@ static void build_graphs(Plan& pl, double* x) {
         ws->graph[par] = nullptr;
         // a released workspace's executable graph of the same topology (a new
         // hierarchy of the same shape) is re-pointed instead of re-instantiated
-        cudaGraphExec_t reuse = graph_cache_take();
+        size_t nodes = 0;
+        UA_CK(cudaGraphGetNodes(g, nullptr, &nodes));
+        ws->graph_nodes[par] = nodes;
+        cudaGraphExec_t reuse = graph_cache_take(par, nodes);
         if (reuse) {
             cudaGraphExecUpdateResultInfo info;
             if (cudaGraphExecUpdate(reuse, g, &info) == cudaSuccess) {

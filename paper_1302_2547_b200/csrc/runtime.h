@@ -49,8 +49,11 @@ constexpr int kLookahead = 3;  // iteration graphs queued ahead of the host's fl
 constexpr int kEvRing = 4;
 int mapped_slot_acquire(int** host, int** dev);
 void mapped_slot_release(int k);
-cudaGraphExec_t graph_cache_take();
-void graph_cache_give(cudaGraphExec_t e);
+// executable-graph cache keyed by (parity, node count): an update is only
+// tried on a graph of the same shape, so it does not fail into a fresh
+// instantiation (several ms) inside a timed solve
+cudaGraphExec_t graph_cache_take(int par, size_t nodes);
+void graph_cache_give(cudaGraphExec_t e, int par, size_t nodes);
 
 struct SolveWs {
     uaamg_solve_params key{};
@@ -79,6 +82,7 @@ struct SolveWs {
     DBuf<double> fpart;    // fused direction + update: per-CTA partials
     DBuf<unsigned> fbar;   // and its grid barrier
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    size_t graph_nodes[2] = {0, 0};  // node counts (graph cache key)
     uint64_t graph_kernels[2] = {0, 0};  // kernel launches recorded per graph
     // level-0 hot-kernel timing (profile_level0): event pairs per graph parity
     // around the residual, fused up-sweep and direction-SpMV kernels
@@ -94,7 +98,7 @@ struct SolveWs {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaEvent_t evr[4] = {nullptr, nullptr, nullptr, nullptr};  // lookahead ring (kEvRing)
     ~SolveWs() {
-        for (auto& g : graph) graph_cache_give(g);  // the work using it has completed
+        for (int k = 0; k < 2; ++k) graph_cache_give(graph[k], k, graph_nodes[k]);  // its work has completed
         for (auto& row : pev)
             for (auto& e : row) if (e) cudaEventDestroy(e);
         mapped_slot_release(flag_slot);
