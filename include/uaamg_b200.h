@@ -128,7 +128,11 @@ typedef struct {
     int singular;           /* -1 auto (detect_singular), 0/1 forced             */
     int borrow;             /* 1: level 0 aliases the caller's arrays (they must
                                outlive the hierarchy, as the reference's Level 0
-                               holds the caller's matrix); 0: copied          */
+                               holds the caller's matrix, and each must have
+                               64 readable bytes past its last element: the
+                               level-0 tile kernel's bulk copies round slices
+                               up to 16-byte granules); arrays that are not
+                               16-byte aligned are copied anyway; 0: copied */
 } uaamg_setup_params;
 
 /* U/hierarchy.py:120-153.  Matrix arrays are device pointers, copied into
@@ -174,9 +178,6 @@ typedef struct {
     int max_iters;           /* npcg_solve max_iters                          */
     int use_graphs;          /* 1: replay one CUDA graph per iteration        */
     int profile_level0;      /* 1: time level-0 smoother kernels (events)     */
-    int engine_rows;         /* levels >= 1 with at most this many rows run in
-                                the persistent coarse engine (one cooperative
-                                launch per cycle entry); 0 off, < 0 default   */
 } uaamg_solve_params;
 
 typedef struct {

@@ -45,7 +45,7 @@ class LevelView(ctypes.Structure):
 class SolveParams(ctypes.Structure):
     _fields_ = [("kcycle", _i), ("inner_krylov_steps", _i), ("pre_sweeps", _i), ("post_sweeps", _i),
                 ("smoother_l1", _i), ("omega", _d), ("tol", _d), ("max_iters", _i), ("use_graphs", _i),
-                ("profile_level0", _i), ("engine_rows", _i)]
+                ("profile_level0", _i)]
 
 
 class SolveResult(ctypes.Structure):

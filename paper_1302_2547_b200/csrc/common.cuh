@@ -200,8 +200,12 @@ __device__ __forceinline__ double block_sum(double v, double* sm /* >= NT/32 + 1
 // to partials[k*nb + block]; the last block to arrive (atomic ticket) sums
 // the partials in block order and calls fin(tot) on thread 0, then rearms
 // the ticket.  Must be called by all threads of every block of the launch.
+// lval/nlong: per-long-row values (stride 2) of a CSR operation whose long
+// rows were finished by arrival-order-dependent warps, folded after the
+// block partials in row order.
 template <int K, int NT = kThreads, class F>
-__device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* partials, unsigned* ticket, F&& fin) {
+__device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* partials, unsigned* ticket, F&& fin,
+                                                   const double* lval = nullptr, int nlong = 0) {
     __shared__ double sm[NT / 32 + 1];
     __shared__ bool last;
     double tot[K];
@@ -221,6 +225,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* parti
     for (int k = 0; k < K; ++k) {
         double s = 0.0;
         for (int b = threadIdx.x; b < nb; b += NT) s += __ldcg(partials + k * nb + b);
+        for (int r = threadIdx.x; r < nlong; r += NT) s += __ldcg(lval + 2 * r + k);
         tot[k] = block_sum<NT>(s, sm);
     }
     if (threadIdx.x == 0) {

@@ -20,6 +20,9 @@
 // adds the row's partials in piece order and runs the epilogue --
 // deterministic, not reference-ordered (the solve's parity bar is the 1e-10
 // residual-history tolerance).  The lanes of the owning group skip such rows.
+// A long row's share of a grid reduction is stored per row (G.lval) and
+// folded in row order after the block partials, never into the partial of
+// whichever block happened to finish the row.
 #pragma once
 #include "solve_ops.cuh"
 
@@ -124,7 +127,21 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
             acc = warp_sum(acc);
             if (lane == 0) {
                 G.ticket[lr] = 0u;
-                epi.row(row, acc, src);
+                if constexpr (Epi::K > 0) {
+                    // which warp finishes a long row depends on arrival order:
+                    // its reduced values go to the row's own slot (folded in
+                    // row order by the reduction's finisher), not into this
+                    // thread's partials -- same bits on every run
+                    Epi e1 = epi;
+                    e1.clear();
+                    e1.row(row, acc, src);
+                    double d[Epi::K];
+                    e1.vals(d);
+#pragma unroll
+                    for (int k = 0; k < Epi::K; ++k) G.lval[kMaxLongK * lr + k] = d[k];
+                } else {
+                    epi.row(row, acc, src);
+                }
             }
         }
     }
@@ -168,7 +185,7 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, S
         epi.vals(v);
         grid_reduce_finish<Epi::K>(v, epi.red.partials, epi.red.ticket, [&](const double (&t)[Epi::K]) {
             if (!xpublish(epi.red, t)) epi.fin(t);
-        });
+        }, G.lval, G.nlong);
     }
 }
 
@@ -215,6 +232,10 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
         for (int b = threadIdx.x; b < nb; b += 32) {
             t0 += __ldcg(part + b);
             t1 += __ldcg(part + nb + b);
+        }
+        for (int r = threadIdx.x; r < G.nlong; r += 32) {  // long rows, row order
+            t0 += __ldcg(G.lval + kMaxLongK * r);
+            t1 += __ldcg(G.lval + kMaxLongK * r + 1);
         }
         t0 = warp_sum(t0);
         t1 = warp_sum(t1);

@@ -18,6 +18,8 @@ struct Groups {
     const int* pbase = nullptr;  // per long row: first partial slot (nlong + 1)
     unsigned* ticket = nullptr;  // per long row, zero between uses
     double* part = nullptr;      // np partial sums
+    int nlong = 0;               // long rows (pieces grouped by row)
+    double* lval = nullptr;      // per long row: its epilogue's reduced values (kMaxLongK each)
     int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per 128-row tile
     __host__ __device__ int units() const { return ng + np; }
 };
@@ -35,18 +37,19 @@ struct GroupBuf {
     DBuf<int> pbase;
     DBuf<unsigned> ticket;
     DBuf<double> part;
+    DBuf<double> lval;
     Groups g;
 };
 // long_min: rows with more entries become pieces (solve path)
 // rows [base, base + n) of a CSR with global row_ptr rp
 void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s, int base = 0);
 constexpr int kSolveLongMin = 256;
+// reduced values per long row kept for the deterministic fold (max Epi::K)
+constexpr int kMaxLongK = 2;
 // levels with at least this many rows take the TMA-pipelined tile kernel
 constexpr int kTmaMinRows = 65536;
 // max nonzeros over 128-row tiles (for the TMA path)
 int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0);
-
-struct Op;  // one recorded engine phase (ops.cuh)
 
 // fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
 struct BetaReq {
@@ -56,12 +59,10 @@ struct BetaReq {
     const int* have;  // nullptr: always
 };
 
-// Where a solve operation goes: launched on a stream, or -- rec != nullptr --
-// appended to an op list the persistent engine interprets (engine.cu).
+// Where a solve operation is launched.
 struct Exec {
     cudaStream_t s = 0;
-    std::vector<Op>* rec = nullptr;
-    Exec(cudaStream_t st = 0, std::vector<Op>* r = nullptr) : s(st), rec(r) {}
+    Exec(cudaStream_t st = 0) : s(st) {}
 };
 
 constexpr int kMaxInner = 16;

@@ -113,7 +113,7 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.step = step; e.red = {rs.partials, rs.ticket};
     SrcDir src{};
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = nullptr; src.have_static = have_prev;
-    if (G.tma_cap > 0 && !ex.rec) {
+    if (G.tma_cap > 0) {
         // large level: p first, then a plain-gather SpMV (same arithmetic)
         BodyDirP bp{};
         bp.src = src; bp.p = p; bp.g = &st->gate[step];
@@ -129,7 +129,7 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
                            RedScratch rs, double* part, unsigned* bar, Exec ex) {
     static const bool no_fuse = getenv("UAAMG_NO_DIR_FUSE") != nullptr;  // A/B diagnostics
-    if (ex.rec || G.tma_cap > 0 || no_fuse) {
+    if (G.tma_cap > 0 || no_fuse) {
         launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
         launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex);
         return;
@@ -248,6 +248,7 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
     out.pbase.alloc(m + 1, s);
     out.ticket.alloc(m, s);
     out.part.alloc(pcs.size(), s);
+    out.lval.alloc((size_t)kMaxLongK * m, s);
     UA_CK(cudaMemcpyAsync(out.piece.p, pcs.data(), sizeof(int4) * pcs.size(), cudaMemcpyHostToDevice, s));
     UA_CK(cudaMemcpyAsync(out.pbase.p, pbase.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, s));
     UA_CK(cudaMemsetAsync(out.ticket.p, 0, sizeof(unsigned) * m, s));
@@ -257,6 +258,8 @@ void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_
     out.g.pbase = out.pbase.p;
     out.g.ticket = out.ticket.p;
     out.g.part = out.part.p;
+    out.g.nlong = m;
+    out.g.lval = out.lval.p;
 }
 
 // ---- smoother diagonal (U/solvers.py:69-81, K/numba_backend.py:59-84)
@@ -444,10 +447,6 @@ __global__ void k_dense_solve(int n, const double* __restrict__ M, const double*
 }
 void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, Exec ex) {
     if (n == 0) return;
-    if (ex.rec) {
-        record_dense(*ex.rec, DenseArgs{Minv, b, x, gate, n});
-        return;
-    }
     UA_LAUNCH_PDL(k_dense_solve, cdiv(n, 8), 256, 0, ex.s, n, Minv, b, x, gate);
 }
 

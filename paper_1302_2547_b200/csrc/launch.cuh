@@ -1,11 +1,9 @@
 // launch.cuh -- host-side dispatch of the solve functors: run_stream (CSR
-// row operations: TMA tiles on large levels, warp groups otherwise, or an
-// engine op when recording) and run_map (elementwise + reductions), plus the
+// row operations: TMA tiles on large levels, warp groups otherwise) and run_map (elementwise + reductions), plus the
 // cross-rank reduction finish of the sharded solve (shard.cu).
 #pragma once
 #include "csr_group.cuh"
 #include "csr_tma.cuh"
-#include "ops.cuh"
 
 namespace uaamg {
 
@@ -38,10 +36,6 @@ inline int map_grid(int n) {
 
 template <class Body>
 void run_map(int n, const Body& body, Exec ex) {
-    if (ex.rec) {
-        record_map(*ex.rec, n, body);
-        return;
-    }
     UA_LAUNCH_PDL((k_map<Body>), map_grid(n), kThreads, 0, ex.s, n, body);
 }
 
@@ -52,10 +46,6 @@ void run_map(int n, const Body& body, Exec ex);
 
 template <class Src, class Epi, bool Unit>
 inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
-    if (ex.rec) {
-        record_csr<Src, Epi, Unit>(*ex.rec, A, G, src, epi);
-        return;
-    }
     // an empty range still launches when it must publish a (zero) reduction
     if (G.units() == 0) {
         if constexpr (Epi::K == 0) return;

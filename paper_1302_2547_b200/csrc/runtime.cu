@@ -25,7 +25,6 @@
 #include <vector>
 
 #include "csr_tma.cuh"
-#include "engine.h"
 #include "setup.h"
 
 #include "runtime.h"
@@ -238,7 +237,10 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
     auto L0 = std::make_unique<Level>();
     L0->n = n;
     L0->nnz = nnz;
-    if (P.borrow) {
+    // the TMA tile kernel bulk-copies level-0 slices: sources must be
+    // 16-byte aligned (borrowed arrays that are not are copied instead)
+    auto a16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    if (P.borrow && a16(rp) && a16(ci) && a16(av)) {
         // level 0 aliases the caller's arrays (U/hierarchy.py: Level 0 holds A)
         L0->rp.adopt_view(const_cast<int*>(rp), n + 1);
         L0->ci.adopt_view(const_cast<int*>(ci), std::max(nnz, 1ll));
@@ -382,8 +384,7 @@ void mapped_slot_release(int k) {
     g_slot_free.push_back(k);
 }
 
-std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, bool engine,
-                                  int mat_levels) {
+std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels) {
     std::unique_ptr<SolveWs> ws(new SolveWs());
     ws->key = p;
     static const bool wsprof = getenv("UAAMG_WS_PROF") != nullptr;  // diagnostics
@@ -466,47 +467,8 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
     for (auto& e : ws->evr) UA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (p.inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
     wmark("outer");
-    // persistent coarse engine from the first level (>= 1) small enough
-    const long long erows = p.engine_rows < 0 ? kEngDefaultRows : p.engine_rows;
-    ws->Lc = -1;
-    if (engine && erows > 0)
-        for (int l = 1; l < nl; ++l)
-            if (h->levels[l]->n <= erows) { ws->Lc = l; break; }
-    if (ws->Lc > 0) {
-        // record cycle(Lc) / fcg(Lc) -- exactly what Plan::cycle(Lc - 1)
-        // would launch -- as the engine's op list
-        std::vector<Op> ops;
-        Plan rp{h, ws.get(), p, s};
-        rp.rec = &ops;
-        const int L0 = ws->Lc;
-        LevelWs& C = ws->lev[L0];
-        const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || L0 == nl - 1;
-        if (direct) rp.cycle(L0, C.rhs.p, C.e.p, nullptr);
-        else rp.fcg(L0, C.rhs.p, C.xf.p, nullptr, !h->singular);
-        // schedule: small ops on one cluster; a grid barrier before the
-        // first big op after small ones
-        long long small_rows = kEngSmallRows;
-        if (const char* e = getenv("UAAMG_ENGINE_SMALL")) small_rows = atoll(e);
-        for (size_t k = 0; k < ops.size(); ++k) {
-            ops[k].small = ops[k].n <= small_rows ? 1 : 0;
-            ops[k].sync_before = (!ops[k].small && k > 0 && ops[k - 1].small) ? 1 : 0;
-        }
-        ws->neops = (int)ops.size();
-        ws->hops = ops;
-        if (getenv("UAAMG_ENGINE_PROF")) {
-            ws->eprof.alloc(ops.size() + 1, s);
-            ws->prof_acc.assign(ops.size(), 0.0);
-        }
-        ws->eops.alloc(std::max<size_t>(ops.size(), 1), s);
-        UA_CK(cudaMemcpyAsync(ws->eops.p, ops.data(), sizeof(Op) * ops.size(), cudaMemcpyHostToDevice, s));
-        ws->epart.alloc(4 * (size_t)kEngK * engine_grid(), s);
-        ws->ebar.alloc(2, s);
-        UA_CK(cudaMemsetAsync(ws->ebar.p, 0, 2 * sizeof(unsigned), s));
-        UA_CK(cudaStreamSynchronize(s));  // ops vector is a host temporary
-    }
-    wmark("engine");
     // the level above the coarsest as one cluster kernel (tail.cu)
-    if (!getenv("UAAMG_NO_TAIL") && ws->Lc < 0 && !sing && nl >= 3 && p.pre_sweeps <= 1 && p.post_sweeps <= 1) {
+    if (!getenv("UAAMG_NO_TAIL") && !sing && nl >= 3 && p.pre_sweeps <= 1 && p.post_sweeps <= 1) {
         const int Lt = nl - 2;
         const Level& T = *h->levels[Lt];
         const Level& U = *h->levels[Lt - 1];
@@ -548,12 +510,11 @@ void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s) 
     const bool same = ws && ws->ready && ws->key.kcycle == p.kcycle &&
                       ws->key.inner_krylov_steps == p.inner_krylov_steps && ws->key.pre_sweeps == p.pre_sweeps &&
                       ws->key.post_sweeps == p.post_sweeps && ws->key.smoother_l1 == p.smoother_l1 &&
-                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters &&
-                      ws->key.engine_rows == p.engine_rows;
+                      ws->key.omega == p.omega && ws->key.max_iters >= p.max_iters;
     if (same) return;
     if (ws) UA_CK(cudaStreamSynchronize(s));
     ws.reset();
-    ws = build_ws(h, p, s, true, 0);
+    ws = build_ws(h, p, s, 0);
 }
 
 static void build_graphs(Plan& pl, double* x) {
@@ -743,21 +704,6 @@ static int npcg_impl(uaamg_hierarchy* h, const uaamg_solve_params& p, const doub
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     print_tail_prof(ws->tail);
-    if (ws->eprof.p && ws->neops > 0) {
-        // diagnostics: per-op durations of the last engine run, by (kind, rows)
-        std::vector<unsigned long long> t(ws->neops + 1);
-        UA_CK(cudaMemcpy(t.data(), ws->eprof.p, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
-        std::map<std::pair<int, int>, std::pair<int, double>> agg;
-        for (int k = 0; k < ws->neops; ++k) {
-            auto& e = agg[{ws->hops[k].kind, ws->hops[k].n}];
-            e.first += 1;
-            e.second += (double)(t[k + 1] - t[k]) * 1e-3;
-        }
-        fprintf(stderr, "engine ops %d, total %.1f us\n", ws->neops, (double)(t[ws->neops] - t[0]) * 1e-3);
-        for (auto& kv : agg)
-            fprintf(stderr, "  kind %2d n %8d: %4d ops %9.1f us (%.2f us/op)\n", kv.first.first, kv.first.second,
-                    kv.second.first, kv.second.second, kv.second.second / kv.second.first);
-    }
     res->iterations = hst.iters;
     res->solve_seconds = ms * 1e-3;
     res->l0_kernel_launches = prof_n;

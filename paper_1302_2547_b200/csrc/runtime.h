@@ -14,7 +14,6 @@
 #include <vector>
 
 #include "csr_tma.cuh"
-#include "engine.h"
 #include "setup.h"
 #include "tail.h"
 
@@ -68,16 +67,6 @@ struct SolveWs {
     DBuf<int> bad_row;
     // outer vectors
     DBuf<double> r, z, p0, p1, ap0, ap1, hist, bproj;
-    // persistent coarse engine: levels >= Lc (Lc < 0: off)
-    int Lc = -1;
-    DBuf<Op> eops;
-    int neops = 0;
-    std::vector<Op> hops;                 // host copy of the op list (diagnostics)
-    DBuf<unsigned long long> eprof;       // UAAMG_ENGINE_PROF=1: op start times
-    std::vector<double> prof_acc;         // per-op accumulated seconds
-    int prof_runs = 0;
-    DBuf<double> epart;
-    DBuf<unsigned> ebar;
     TailPlan tail;         // the level above the coarsest in one cluster (tail.cu)
     DBuf<double> fpart;    // fused direction + update: per-CTA partials
     DBuf<unsigned> fbar;   // and its grid barrier
@@ -160,8 +149,7 @@ struct Plan {
     uaamg_solve_params p;
     cudaStream_t s;
     int prof = -1;  // >= 0: record level-0 timing events of this parity
-    std::vector<Op>* rec = nullptr;  // recording the engine's op list
-    Exec ex() const { return Exec(s, rec); }
+    Exec ex() const { return Exec(s); }
     void mark(int k) {
         // External: a real event-record node inside the captured graph (a
         // plain cudaEventRecord during capture only orders nodes)
@@ -233,7 +221,7 @@ struct Plan {
         // the coarse flexible CG's ||r_c|| / gate[0] come out of the restriction
         const bool begun = !direct && !sing();
         // the tail kernel restricts, solves and returns the coarse correction
-        const bool tail = ws->tail.on && l + 1 == ws->tail.Lt && rec == nullptr;
+        const bool tail = ws->tail.on && l + 1 == ws->tail.Lt;
         if (!tail) {
             launch_restrict(L.nc, L.agg_ptr.p, L.members.p, L.mgroups(), W.r.p, C.rhs.p, gate, ex(),
                             begun ? ws->fcg.p + l + 1 : nullptr, rs());
@@ -247,10 +235,6 @@ struct Plan {
             launch_tail(ws->tail, W.r.p, gate, o, u0, s);
             ec = o;
             ec_valid = u0;
-        } else if (l + 1 == ws->Lc) {
-            engine(gate);
-            ec = direct ? C.e.p : C.xf.p;
-            if (!direct) ec_valid = &ws->fcg.p[l + 1].upd[0];
         } else if (direct) {
             cycle(l + 1, C.rhs.p, C.e.p, gate);
             ec = C.e.p;
@@ -300,18 +284,6 @@ struct Plan {
         }
         if (sing()) launch_project_mean(L.n, out, ws->sums.p + 4 * l + 3, gate, rs(), ex());
         return fb != nullptr;
-    }
-
-    // the whole recursion from level Lc down in one cooperative launch
-    void engine(const int* gate) {
-        EngineArgs a;
-        a.ops = ws->eops.p;
-        a.nops = ws->neops;
-        a.gate = gate;
-        a.partials = ws->epart.p;
-        a.bar = ws->ebar.p;
-        a.prof = ws->eprof.p;
-        launch_engine(a, s);
     }
 
     // U/solvers.py:160-187
@@ -367,9 +339,8 @@ struct Plan {
 
 void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s);
 cudaStream_t library_stream();
-// a fresh solve workspace; engine: record the persistent-engine op list;
-// levels < mat_levels materialise the pre-smoothed / prolongated iterates
-std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, bool engine,
-                                  int mat_levels);
+// a fresh solve workspace; levels < mat_levels materialise the
+// pre-smoothed / prolongated iterates
+std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels);
 
 }  // namespace uaamg

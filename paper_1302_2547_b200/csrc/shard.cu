@@ -34,6 +34,8 @@ namespace uaamg {
 
 namespace {
 
+constexpr int kSlotK = 2;  // max values per cross-rank reduction (Epi::K)
+
 enum VRole { V_R, V_RHS, V_E, V_TA, V_TB, V_XUP, V_XF, V_RF, V_Z, V_P0, V_P1, V_AP0, V_AP1,
              T_R, T_Z, T_P0, T_P1, T_AP0, T_AP1, T_X, T_B };
 struct VRef {
@@ -64,7 +66,7 @@ struct Sharded {
     std::vector<std::unique_ptr<SolveWs>> ws;  // [rank] (null for remote ranks)
     std::vector<SLevel> lv;
     std::vector<DBuf<double>> xr, br;  // per rank: iterate and right-hand side
-    DBuf<double> slots;                // virtual: P x (kEngK * P)
+    DBuf<double> slots;                // virtual: P x (kSlotK * P)
     DBuf<double*> slot_tab;            // P pointers: slot array of every rank
     // multi-process: every vector a peer may read lives in one cudaMalloc
     // arena per rank (same layout everywhere), exported by CUDA IPC
@@ -88,7 +90,7 @@ struct Sharded {
     int nrows(int r, int l) const { return lv[l].part.b[r + 1] - lv[l].part.b[r]; }
     RedScratch rs(int r) const { return RedScratch{ws[r]->partials.p, ws[r]->ticket.p}; }
     const double* slot(int r) const {
-        return rank < 0 ? slots.p + (size_t)r * kEngK * P : reinterpret_cast<const double*>(arena + slots_off);
+        return rank < 0 ? slots.p + (size_t)r * kSlotK * P : reinterpret_cast<const double*>(arena + slots_off);
     }
     // multi-process: cross-device barrier before an op reads what peers wrote
     void sync();
@@ -495,7 +497,7 @@ std::unique_ptr<Sharded> sharded_build(uaamg_hierarchy* h, const uaamg_solve_par
     if (S.Ls == 0) throw Error(UAAMG_EUNSUPPORTED, "sharded solve needs at least two levels");
     S.lv.resize(nl);
     S.ws.resize(P);
-    for (int r : S.mine) S.ws[r] = build_ws(h, p, s, false, S.Ls);
+    for (int r : S.mine) S.ws[r] = build_ws(h, p, s, S.Ls);
     S.lv[0].part = level0_part(h->levels[0]->n, P);
     for (int l = 0; l < S.Ls; ++l) {
         S.lv[l].sharded = true;
@@ -532,9 +534,9 @@ std::unique_ptr<Sharded> sharded_build(uaamg_hierarchy* h, const uaamg_solve_par
     }
     S.slot_tab.alloc(P, s);
     if (rank < 0) {
-        S.slots.alloc((size_t)P * kEngK * P, s);
+        S.slots.alloc((size_t)P * kSlotK * P, s);
         std::vector<double*> tab(P);
-        for (int q = 0; q < P; ++q) tab[q] = S.slots.p + (size_t)q * kEngK * P;
+        for (int q = 0; q < P; ++q) tab[q] = S.slots.p + (size_t)q * kSlotK * P;
         UA_CK(cudaMemcpyAsync(S.slot_tab.p, tab.data(), sizeof(double*) * P, cudaMemcpyHostToDevice, s));
         UA_CK(cudaStreamSynchronize(s));
         return Sp;
@@ -560,7 +562,7 @@ std::unique_ptr<Sharded> sharded_build(uaamg_hierarchy* h, const uaamg_solve_par
         return o;
     };
     for (auto& e : shared) S.off[e.first] = take(e.second->n * sizeof(double));
-    S.slots_off = take(sizeof(double) * kEngK * P);
+    S.slots_off = take(sizeof(double) * kSlotK * P);
     S.flags_off = take(sizeof(unsigned) * 32 * P);
     S.arena_bytes = bytes;
     UA_CK(cudaStreamSynchronize(s));

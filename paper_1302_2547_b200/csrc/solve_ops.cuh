@@ -28,6 +28,7 @@ __device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.globa
 //   __device__ void row(int i, double acc, const Src& src);   // per row
 //   static constexpr int K;                                   // reduced values
 //   __device__ void vals(double (&v)[K]) const;               // this thread's partials
+//   __device__ void clear();                                  // zero this thread's partials
 //   __device__ void fin(const double (&t)[K]);                // once, with the totals
 //   __device__ bool gate() const;                             // false: skip
 //   __device__ void off();                                    // gate false: clear produced flags
@@ -201,6 +202,7 @@ struct EpiResidSum {
         s0 += v;
     }
     __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void clear() { s0 = 0.0; }
     __device__ void fin(const double (&t)[1]) {
         *rc = t[0];
         *ec = minv[0] * t[0];
@@ -250,6 +252,7 @@ struct EpiSweepBeta {
         s0 += o * apprev[i];
     }
     __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void clear() { s0 = 0.0; }
     __device__ void fin(const double (&t)[1]) {
         if (have == nullptr || *have) *beta = -t[0] / *pap;
     }
@@ -277,6 +280,7 @@ struct EpiDirFcg {
         s1 += pi * r[i];
     }
     __device__ void vals(double (&v)[2]) const { v[0] = s0; v[1] = s1; }
+    __device__ void clear() { s0 = 0.0; s1 = 0.0; }
     __device__ void fin(const double (&t)[2]) {
         // U/solvers.py:178-181: break if p'Ap <= 0, else alpha = p'r / p'Ap
         st->pap = t[0];
@@ -307,6 +311,7 @@ struct EpiDirNpcg {
         s1 += pi * r[i];
     }
     __device__ void vals(double (&v)[2]) const { v[0] = s0; v[1] = s1; }
+    __device__ void clear() { s0 = 0.0; s1 = 0.0; }
     __device__ void fin(const double (&t)[2]) {
         // U/solvers.py:230-237: breakdown if p'Ap <= 0
         st->pap = t[0];
@@ -354,6 +359,7 @@ struct EpiRestrictBegin {
         s0 += acc * acc;
     }
     __device__ void vals(double (&v)[1]) const { v[0] = s0; }
+    __device__ void clear() { s0 = 0.0; }
     __device__ void fin(const double (&t)[1]) {
         const double nb = sqrt(t[0]);
         st->bnorm = nb;

@@ -44,6 +44,50 @@ def to_device(a, dtype):
     return torch.from_numpy(arr).to(device=cuda_device(), non_blocking=False)
 
 
+# Bytes past the end of a level-0 array the TMA tile kernel may read: its
+# bulk copies round every slice up to 16-byte granules
+# (include/uaamg_b200.h, uaamg_setup_params.borrow).
+TAIL_SLACK = 64
+
+
+def device_empty(n, dtype):
+    """Uninitialised device tensor of ``n`` elements with TAIL_SLACK readable
+    bytes after the last one (a view of a slightly larger allocation)."""
+    dt = _TORCH[np.dtype(dtype)]
+    item = np.dtype(dtype).itemsize
+    full = torch.empty(int(n) + -(-TAIL_SLACK // item), dtype=dt, device=cuda_device())
+    return full[: int(n)]
+
+
+def to_device_padded(a, dtype):
+    """to_device into a device_empty buffer (borrowable by uaamg_setup)."""
+    src = to_device(a, dtype) if isinstance(a, torch.Tensor) else None
+    if src is not None and borrowable(src, dtype):
+        return src
+    if src is None:
+        arr = np.ascontiguousarray(a, dtype=dtype)
+        out = device_empty(arr.shape[0], dtype)
+        out.copy_(torch.from_numpy(arr if arr.flags.writeable else arr.copy()))
+        return out
+    out = device_empty(src.shape[0], dtype)
+    out.copy_(src)
+    return out
+
+
+def borrowable(t, dtype):
+    """Can uaamg_setup alias ``t`` as a level-0 array: 1-D, contiguous, of
+    ``dtype``, on the current device, 16-byte aligned (cp.async.bulk source
+    alignment) and with TAIL_SLACK bytes of its storage after the end."""
+    if not isinstance(t, torch.Tensor) or t.dtype != _TORCH[np.dtype(dtype)] or t.dim() != 1:
+        return False
+    if not t.is_cuda or t.device != cuda_device() or not t.is_contiguous():
+        return False
+    if t.data_ptr() % 16:
+        return False
+    end = (t.storage_offset() + t.numel()) * t.element_size()
+    return t.untyped_storage().nbytes() - end >= TAIL_SLACK
+
+
 def ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -86,23 +130,35 @@ class _CsrOwner:
 class DeviceCSR:
     """Device CSR matrix: int32 row_ptr/col, float64 val (square)."""
 
-    __slots__ = ("n_rows", "n_cols", "row_ptr", "col", "val")
+    __slots__ = ("n_rows", "n_cols", "row_ptr", "col", "val", "lib_owned")
 
-    def __init__(self, n_rows, n_cols, row_ptr, col, val):
+    def __init__(self, n_rows, n_cols, row_ptr, col, val, lib_owned=False):
         self.n_rows = int(n_rows)
         self.n_cols = int(n_cols)
         self.row_ptr, self.col, self.val = row_ptr, col, val
+        self.lib_owned = lib_owned  # arrays are library buffers (tail slack guaranteed)
+
+    def borrowable(self):
+        """Level 0 of a hierarchy may alias these arrays (no copy)."""
+        if self.lib_owned:
+            ok = all(isinstance(t, torch.Tensor) and t.is_contiguous() and t.data_ptr() % 16 == 0
+                     for t in (self.row_ptr, self.col, self.val))
+            return ok and self.row_ptr.dtype == torch.int32 and self.col.dtype == torch.int32 \
+                and self.val.dtype == torch.float64
+        return borrowable(self.row_ptr, np.int32) and borrowable(self.col, np.int32) \
+            and borrowable(self.val, np.float64)
 
     @classmethod
     def from_host(cls, a):
         if a.nnz >= 2 ** 31 or a.n_rows >= 2 ** 31:
             raise ValueError("matrix too large for int32 device indices")
-        return cls(a.n_rows, a.n_cols, to_device(a.indptr, np.int32), to_device(a.indices, np.int32),
-                   to_device(a.data, np.float64))
+        return cls(a.n_rows, a.n_cols, to_device_padded(a.indptr, np.int32), to_device_padded(a.indices, np.int32),
+                   to_device_padded(a.data, np.float64))
 
     @classmethod
     def from_arrays(cls, n, row_ptr, col, val):
-        return cls(n, n, to_device(row_ptr, np.int32), to_device(col, np.int32), to_device(val, np.float64))
+        return cls(n, n, to_device_padded(row_ptr, np.int32), to_device_padded(col, np.int32),
+                   to_device_padded(val, np.float64))
 
     @classmethod
     def _from_lib(cls, handle):
@@ -116,7 +172,8 @@ class DeviceCSR:
                          ctypes.byref(ci), ctypes.byref(av))
         owner = _CsrOwner(handle)
         return cls(nr.value, nc.value, view(rp.value, nr.value + 1, np.int32, owner),
-                   view(ci.value, nnz.value, np.int32, owner), view(av.value, nnz.value, np.float64, owner))
+                   view(ci.value, nnz.value, np.int32, owner), view(av.value, nnz.value, np.float64, owner),
+                   lib_owned=True)
 
     @classmethod
     def from_coo(cls, n_rows, n_cols, rows, cols, vals):

@@ -67,7 +67,7 @@ def npcg_solve_distributed(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, 
     if bd.shape != (n,):
         raise ValueError("right-hand side size mismatch")
     x0d = to_device(x0, np.float64) if x0 is not None else None
-    P = _params(cycle_spec, smoother, tol, max_iters, False, 0)
+    P = _params(cycle_spec, smoother, tol, max_iters, False)
     L = _lib.load()
     d = ctypes.c_void_p()
     _lib.check(L.uaamg_dist_create(h._handle, ctypes.byref(P), rank, size, int(shard_rows), ctypes.byref(d)))

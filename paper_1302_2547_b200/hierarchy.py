@@ -14,10 +14,11 @@ import ctypes
 import weakref
 
 import numpy as np
+import torch
 
 from . import _lib
 from .aggregation import Aggregation, AggregationConfig
-from .device import DeviceCSR, ptr, stream, view
+from .device import DeviceCSR, cuda_device, ptr, stream, view
 from .sparse import SparseMatrix
 
 
@@ -84,7 +85,8 @@ class Level:
         if self._dev is None:
             v = self._view()
             self._dev = DeviceCSR(v.n, v.n, view(v.row_ptr, v.n + 1, np.int32, self._h),
-                                  view(v.col, v.nnz, np.int32, self._h), view(v.val, v.nnz, np.float64, self._h))
+                                  view(v.col, v.nnz, np.int32, self._h), view(v.val, v.nnz, np.float64, self._h),
+                                  lib_owned=True)
         return self._dev
 
     @property
@@ -199,10 +201,18 @@ def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0
         raise NotImplementedError("subgraph reshaping (reshape_sweeps > 0) is outside the B200 hot path "
                                   "(SURVEY.md section 8f, rank 4)")
     d = a if isinstance(a, DeviceCSR) else a.device()
+    # level 0 aliases the caller's device arrays when the TMA tile kernel may
+    # read them in place (int32/int32/float64, contiguous, 16-byte aligned,
+    # 64 readable bytes past the end); otherwise the library copies them
+    borrow = d.borrowable()
+    if not borrow and (d.row_ptr.dtype != torch.int32 or d.col.dtype != torch.int32 or d.val.dtype != torch.float64
+                       or d.row_ptr.device != cuda_device()):
+        d = DeviceCSR.from_arrays(d.n_rows, d.row_ptr, d.col, d.val)
+        borrow = True
     P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
                          max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
                          n0=int(n0), max_levels=int(max_levels),
-                         singular=-1 if singular is None else int(bool(singular)), borrow=1)
+                         singular=-1 if singular is None else int(bool(singular)), borrow=int(borrow))
     h = ctypes.c_void_p()
     _lib.check(_lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
                                        ctypes.byref(h), stream()))

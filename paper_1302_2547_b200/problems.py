@@ -128,7 +128,7 @@ def grid3d_device(n, stencil=7, bc="dirichlet", dims=None):
     import torch
 
     from . import _lib
-    from .device import DeviceCSR, cuda_device, ptr, stream
+    from .device import DeviceCSR, device_empty, ptr, stream
 
     if stencil not in (7, 27):
         raise ValueError("stencil must be 7 or 27")
@@ -136,14 +136,13 @@ def grid3d_device(n, stencil=7, bc="dirichlet", dims=None):
         raise ValueError(f"unknown boundary condition {bc!r}")
     nx, ny, nz = dims if dims is not None else (n, n, n)
     N = nx * ny * nz
-    dev = cuda_device()
-    rp = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    rp = device_empty(N + 1, np.int32)
     nnz = ctypes.c_int64()
     L = _lib.load()
     neu = int(bc == "neumann")
     _lib.check(L.uaamg_gen_grid3d(nx, ny, nz, stencil, neu, ptr(rp), None, None, ctypes.byref(nnz), stream()))
-    ci = torch.empty(nnz.value, dtype=torch.int32, device=dev)
-    av = torch.empty(nnz.value, dtype=torch.float64, device=dev)
+    ci = device_empty(nnz.value, np.int32)
+    av = device_empty(nnz.value, np.float64)
     _lib.check(L.uaamg_gen_grid3d(nx, ny, nz, stencil, neu, ptr(rp), ptr(ci), ptr(av), None, stream()))
     return DeviceCSR(N, N, rp, ci, av)
 

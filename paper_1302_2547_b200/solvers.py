@@ -13,7 +13,6 @@ flags.  Inputs may be numpy (host) or torch CUDA tensors; outputs match.
 """
 
 import ctypes
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -72,10 +71,8 @@ class SolveReport:
                 "residual_history": [float(r) for r in self.residual_history], "timings": dict(self.timings)}
 
 
-def _params(spec, smoother, tol=1e-6, max_iters=200, use_graphs=True, engine_rows=None):
-    if engine_rows is None:
-        engine_rows = int(os.environ.get("UAAMG_ENGINE_ROWS", "-1"))
-    return _lib.SolveParams(engine_rows=int(engine_rows), kcycle=int(spec.kind == "kcycle"), inner_krylov_steps=int(spec.inner_krylov_steps),
+def _params(spec, smoother, tol=1e-6, max_iters=200, use_graphs=True):
+    return _lib.SolveParams(kcycle=int(spec.kind == "kcycle"), inner_krylov_steps=int(spec.inner_krylov_steps),
                             pre_sweeps=int(spec.pre_sweeps), post_sweeps=int(spec.post_sweeps),
                             smoother_l1=int(smoother.kind == "l1"), omega=float(smoother.omega), tol=float(tol),
                             max_iters=int(max_iters), use_graphs=int(use_graphs), profile_level0=0)
@@ -133,18 +130,18 @@ def _vec_in(v, n, what):
     return d, host
 
 
-def cycle(h, spec, smoother, level, b, engine_rows=None):
+def cycle(h, spec, smoother, level, b):
     """One multigrid cycle on A_level x = b from a zero guess (device)."""
     lev = h.levels[level]
     n = lev.n
     bd, host = _vec_in(b, n, "cycle right-hand side")
     x = torch.empty(n, dtype=torch.float64, device=bd.device)
-    P = _params(spec, smoother, engine_rows=engine_rows)
+    P = _params(spec, smoother)
     _lib.check(_lib.load().uaamg_cycle(h._handle, ctypes.byref(P), h._offset + level, ptr(bd), ptr(x), stream()))
     return to_host(x) if host else x
 
 
-def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use_graphs=True, engine_rows=None,
+def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use_graphs=True,
                ranks=None, shard_rows=262144):
     """Flexible PCG with one K-/V-cycle per application, on the device."""
     if tol <= 0:
@@ -156,7 +153,7 @@ def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use
     x0d = to_device(x0, np.float64) if x0 is not None else None
     x = torch.empty(n, dtype=torch.float64, device=bd.device)
     hist = np.zeros(int(max_iters) + 1)
-    P = _params(cycle_spec, smoother, tol, max_iters, use_graphs, engine_rows)
+    P = _params(cycle_spec, smoother, tol, max_iters, use_graphs)
     res = _lib.SolveResult()
     if ranks is None:
         rc = _lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), ptr(bd), ptr(x0d), ptr(x),

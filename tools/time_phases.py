@@ -1,5 +1,4 @@
-"""Time setup and solve separately (CUDA events) for a config, with the coarse
-engine at several thresholds.  Usage: python tools/time_phases.py [n] [stencil]"""
+"""Time setup and solve separately (CUDA events) for a config.  Usage: python tools/time_phases.py [n] [stencil]"""
 import os
 import sys
 import time
@@ -40,10 +39,9 @@ def ev_time(fn, reps=3):
 h, ts = ev_time(lambda: U.setup(Ad), reps=int(os.environ.get("SETUP_REPS", "3")))
 print("setup (event s, wall s):", [(round(a, 4), round(b_, 4)) for a, b_ in ts], flush=True)
 print("levels", [(l.n, l.matrix.nnz if hasattr(l.matrix, "nnz") else None) for l in h.levels], flush=True)
-for er in [int(x) for x in os.environ.get("ENGINE_ROWS_LIST", "0,-1,50000,20000").split(",")]:
-    res, ts = ev_time(lambda: U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500,
-                                           engine_rows=er), reps=3)
+if True:
+    res, ts = ev_time(lambda: U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500), reps=3)
     x, rep = res
-    print(f"engine_rows={er}: iters={rep.iterations} solve(event s, wall s)=",
+    print(f"iters={rep.iterations} solve(event s, wall s)=",
           [(round(a, 4), round(b_, 4)) for a, b_ in ts], "device solve_seconds", rep.timings.get("solve_seconds"),
           flush=True)
