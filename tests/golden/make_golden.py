@@ -315,6 +315,12 @@ def main():
         make_hierarchy(U, "wgraph_3000_cap6", A, cfg_kw={"size_cap": 6, "seed": 2}, solves=[("", {})])
     if want("rgg"):
         make_hierarchy(U, "rgg_20000", P.random_geometric(20000, 12.0, 0), solves=[("", {})])
+    if want("rgg_lcc"):
+        # the solvable C3 (largest connected component of the SURVEY 8d RGG)
+        # at 2^18 vertices; the 2^23 size is pinned by the oracle
+        # (tests/golden/make_oracle_fixtures.py)
+        make_hierarchy(U, "rgg_lcc_262144", P.random_geometric(1 << 18, 12.0, 0, largest_component=True),
+                       solves=[("", {})], full=False)
     if want("small"):
         make_hierarchy(U, "g2d_dir_12_n0", P.grid2d(12), setup_kw={"n0": 200}, solves=[("", {})])
         make_hierarchy(U, "g2d_dir_16_ml2", P.grid2d(16), setup_kw={"max_levels": 2}, solves=[("", {})])

@@ -11,7 +11,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 HIERARCHY_CASES = [
     "c1_grid2d_256", "g2d_dir_64", "g2d_dir_64_t5", "g2d_neu_32", "g2d_dir_64_pp2",
     "g2d_aniso_48", "g3d7_16", "g3d27_10", "wgraph_3000", "wgraph_3000_cap6", "rgg_20000",
-    "g2d_dir_12_n0", "g2d_dir_16_ml2",
+    "g2d_dir_12_n0", "g2d_dir_16_ml2", "rgg_lcc_262144",
 ]
 
 # setup kwargs per case (mirrors make_golden.py)
@@ -59,7 +59,8 @@ def problem_for(name):
         ix = g["L0_indices"].astype(np.int64)
         a = g["L0_data"]
     else:
-        builders = {"c2_grid3d7_128": lambda: P.grid3d(128, 7)}
+        builders = {"c2_grid3d7_128": lambda: P.grid3d(128, 7),
+                    "rgg_lcc_262144": lambda: P.random_geometric(1 << 18, 12.0, 0, largest_component=True)}
         A = builders[name]()
         ip, ix, a = A.indptr, A.indices, A.data
     assert sha(ip, ix, a) == str(g["input_sha"]), "input matrix differs from the fixture's"
