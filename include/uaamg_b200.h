@@ -167,6 +167,20 @@ typedef struct {
 } uaamg_level_view;
 int uaamg_hierarchy_level(const uaamg_hierarchy *h, int level, uaamg_level_view *view);
 
+/* CoarseSolver (U/hierarchy.py:31-65).  uaamg_coarse_factor densifies an
+ * n x n CSR matrix on the device and writes into minv (n*n doubles,
+ * row-major, caller-owned) its inverse via Cholesky (*mode = 1) or, when
+ * `singular` is set or the Cholesky factorisation fails (the reference then
+ * sets singular = True), the eigen pseudo-inverse with the reference's
+ * cut 1e-12 * max(lambda_max, 0) (*mode = 2).  uaamg_hierarchy_coarse
+ * returns the hierarchy's own factor of its coarsest level.
+ * uaamg_dense_apply: x = minv b for nrhs right-hand sides (b, x: n x nrhs
+ * row-major, i.e. numpy's (n,) or (n, nrhs)) -- CoarseSolver.solve. */
+int uaamg_coarse_factor(int n, int64_t nnz, const int *row_ptr, const int *col, const double *val, int singular,
+                        double *minv, int *mode, void *stream);
+int uaamg_hierarchy_coarse(const uaamg_hierarchy *h, const double **minv, int *n, int *mode);
+int uaamg_dense_apply(int n, const double *minv, const double *b, int nrhs, double *x, void *stream);
+
 typedef struct {
     int kcycle;              /* CycleSpec.kind: 1 kcycle, 0 vcycle           */
     int inner_krylov_steps;  /* CycleSpec.inner_krylov_steps (2)            */

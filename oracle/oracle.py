@@ -264,7 +264,7 @@ class OracleLevel:
 class OracleHierarchy:
     """Owns an orc_hier*; levels are copied out to numpy on construction."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, copy=True):
         self._h = handle
         L = lib()
         self.singular = bool(L.orc_hier_singular(handle))
@@ -279,7 +279,8 @@ class OracleHierarchy:
             def arr(q, m, t):
                 if m == 0 or not q.value:
                     return np.zeros(0, dtype=np.int64 if t is _i64p else np.float64)
-                return np.ctypeslib.as_array(ctypes.cast(q, t), shape=(m,)).copy()
+                v = np.ctypeslib.as_array(ctypes.cast(q, t), shape=(m,))
+                return v.copy() if copy else v  # views live as long as the handle
 
             ip = arr(ptrs[0], n + 1, _i64p)
             ix = arr(ptrs[1], nnz, _i64p)
@@ -299,7 +300,7 @@ class OracleHierarchy:
 
 
 def setup(indptr, indices, data, seed=0, max_passes=20, size_cap=None, passes_per_level=1,
-          n0=100, max_levels=20, singular=None):
+          n0=100, max_levels=20, singular=None, copy=True):
     """U/hierarchy.py:120-153 on host CSR arrays."""
     ip, ix, a = _i64(indptr), _i64(indices), _f64(data)
     h = lib().orc_setup(ip.shape[0] - 1, _p(ip), _p(ix), _p(a), int(seed), int(max_passes),
@@ -307,7 +308,7 @@ def setup(indptr, indices, data, seed=0, max_passes=20, size_cap=None, passes_pe
                         int(max_levels), -1 if singular is None else int(bool(singular)))
     if not h:
         raise OracleError(_err())
-    return OracleHierarchy(h)
+    return OracleHierarchy(h, copy=copy)
 
 
 @dataclass

@@ -151,11 +151,13 @@ static void sort_i64(i64 *v, i64 m) {
 i64 orc_squared_pattern(i64 n, const i64 *ip, const i64 *ix, i64 **out_ptr, i64 **out_idx) {
     i64 *ptr = (i64 *)calloc((size_t)n + 1, sizeof(i64));
     int nt = omp_get_max_threads();
-    i64 *stamps = (i64 *)malloc(sizeof(i64) * (size_t)n * (size_t)nt);
+    /* per-thread stamps hold row indices (< 2^31 for every config): int32
+     * halves the n * threads footprint (17 GB at 512^3 with 16 threads) */
+    int32_t *stamps = (int32_t *)malloc(sizeof(int32_t) * (size_t)n * (size_t)nt);
     for (i64 s = 0; s < n * (i64)nt; s++) stamps[s] = -1;
 #pragma omp parallel
     {
-        i64 *stamp = stamps + (i64)omp_get_thread_num() * n;
+        int32_t *stamp = stamps + (i64)omp_get_thread_num() * n;
 #pragma omp for schedule(dynamic, 1024)
         for (i64 i = 0; i < n; i++) {
             i64 cnt = 0;
@@ -163,7 +165,7 @@ i64 orc_squared_pattern(i64 n, const i64 *ip, const i64 *ix, i64 **out_ptr, i64 
                 i64 kk = ix[k];
                 for (i64 k2 = ip[kk]; k2 < ip[kk + 1]; k2++) {
                     i64 j = ix[k2];
-                    if (stamp[j] != i) { stamp[j] = i; cnt++; }
+                    if (stamp[j] != (int32_t)i) { stamp[j] = (int32_t)i; cnt++; }
                 }
             }
             ptr[i + 1] = cnt;
@@ -174,7 +176,7 @@ i64 orc_squared_pattern(i64 n, const i64 *ip, const i64 *ix, i64 **out_ptr, i64 
     for (i64 s = 0; s < n * (i64)nt; s++) stamps[s] = -1;
 #pragma omp parallel
     {
-        i64 *stamp = stamps + (i64)omp_get_thread_num() * n;
+        int32_t *stamp = stamps + (i64)omp_get_thread_num() * n;
 #pragma omp for schedule(dynamic, 1024)
         for (i64 i = 0; i < n; i++) {
             i64 pos = ptr[i];
@@ -182,7 +184,7 @@ i64 orc_squared_pattern(i64 n, const i64 *ip, const i64 *ix, i64 **out_ptr, i64 
                 i64 kk = ix[k];
                 for (i64 k2 = ip[kk]; k2 < ip[kk + 1]; k2++) {
                     i64 j = ix[k2];
-                    if (stamp[j] != i) { stamp[j] = i; idx[pos++] = j; }
+                    if (stamp[j] != (int32_t)i) { stamp[j] = (int32_t)i; idx[pos++] = j; }
                 }
             }
             sort_i64(idx + ptr[i], pos - ptr[i]);

@@ -78,6 +78,9 @@ _SIGS = {
     "uaamg_hierarchy_free": (None, [_vp]),
     "uaamg_hierarchy_get_info": (_i, [_vp, ctypes.POINTER(HierarchyInfo)]),
     "uaamg_hierarchy_level": (_i, [_vp, _i, ctypes.POINTER(LevelView)]),
+    "uaamg_coarse_factor": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, ctypes.POINTER(_i), _vp]),
+    "uaamg_hierarchy_coarse": (_i, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
+    "uaamg_dense_apply": (_i, [_i, _vp, _vp, _i, _vp, _vp]),
     "uaamg_npcg_solve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult),
                               _vp]),
     "uaamg_npcg_solve_sharded": (_i, [_vp, ctypes.POINTER(SolveParams), _i, ctypes.c_int64, _vp, _vp, _vp, _vp,

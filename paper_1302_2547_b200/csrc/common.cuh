@@ -145,6 +145,16 @@ constexpr int kLongRow = 64;            // setup kernels: rows longer than this 
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Process-wide caches of device-dependent facts (occupancy, function
+// attributes, pool state, scratch) are indexed by the current device.
+constexpr int kMaxDevices = 16;
+inline int cur_dev() {
+    int d = 0;
+    UA_CK(cudaGetDevice(&d));
+    if (d < 0 || d >= kMaxDevices) throw Error(UAAMG_EUNSUPPORTED, "device ordinal beyond kMaxDevices");
+    return d;
+}
+
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -169,6 +169,8 @@ void launch_check_compatible(int n, const double* b, double* out, int* err_flag,
                              const int* gate, int level, RedScratch rs, Exec ex);
 // dense coarsest solve x = Minv b
 void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, Exec ex);
+// x = Minv b for nrhs right-hand sides (row-major n x nrhs)
+void launch_dense_apply(int n, const double* Minv, const double* b, int nrhs, double* x, cudaStream_t s);
 // ||v||_2 on device into *out (plain, ungated)
 void launch_norm(int n, const double* v, double* out, RedScratch rs, cudaStream_t s);
 // NPCG init: bnorm, history[0], active

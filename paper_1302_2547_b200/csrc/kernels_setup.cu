@@ -338,7 +338,45 @@ struct AggCoop {
     int* ctl;  // [0..2] centers / pass slot, [3..5] remaining / pass slot, [6..8] changed / iteration slot,
                // [9] passes, [10] leftover, [11..13] |U'| / pass slot, [14..15] |H| / pass parity
     unsigned long long* prof;  // diagnostics (UAAMG_AGG_PROF): per pass {t_start, |U|, |H|, admission iterations}
+    const int* symc;  // k_pattern_sym: {upper entries without a mirror, upper count, lower count}
 };
+
+// Structural symmetry of A's pattern: the admission sweeps'
+// shortcut (admitting j's same-owner neighbours when j is admitted) relies on
+// nb in row(j) => j in row(nb); the reference only tests row(j) itself
+// (K/numba_backend.py:256-266).  Warp per row: every upper entry (i, j > i)
+// looks for i in row j (binary search); with every upper entry mirrored and
+// as many lower as upper entries, the pattern is symmetric.
+__global__ void k_pattern_sym(Csr A, int* symc) {
+    const int lane = threadIdx.x & 31;
+    int miss = 0, up = 0, lo = 0;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A.n; i += (gridDim.x * blockDim.x) >> 5) {
+        const int e0 = A.rp[i], e1 = A.rp[i + 1];
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const int j = __ldg(A.ci + e);
+            if (j < i) { ++lo; continue; }
+            if (j == i) continue;
+            ++up;
+            int a = __ldg(A.rp + j), b = __ldg(A.rp + j + 1);
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (__ldg(A.ci + m) < i) a = m + 1; else b = m;
+            }
+            if (!(a < __ldg(A.rp + j + 1) && __ldg(A.ci + a) == i)) ++miss;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        miss += __shfl_xor_sync(0xffffffffu, miss, o);
+        up += __shfl_xor_sync(0xffffffffu, up, o);
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    if (lane == 0 && (miss | up | lo)) {
+        if (miss) atomicAdd(symc, miss);
+        atomicAdd(symc + 1, up);
+        atomicAdd(symc + 2, lo);
+    }
+}
 
 __device__ __forceinline__ void warp_keymax(double& s, int& i) {
 #pragma unroll
@@ -738,6 +776,7 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
         // fixpoint (and so the result) is the same; grid.sync() between
         // sweeps makes every earlier admission visible.
         uint8_t* adm = g.adm;
+        const bool sym = g.symc[0] == 0 && g.symc[1] == g.symc[2];  // shortcut valid
         while (true) {
             const int slot = itg % 3;
             if (tid == 0) ctl[6 + (itg + 1) % 3] = 0;
@@ -763,7 +802,7 @@ __device__ __forceinline__ void k_aggregate_body(const AggCoop& g) {
                     // through same-owner vertices, so admitting them now only
                     // shortens the sweep chain; owner == a current center
                     // implies the vertex is in U)
-                    if (f) {
+                    if (f && sym) {
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
                             if (!av[q] && ov[q] == c && nb[q] != c && nb[q] != j) adm[nb[q]] = 1;
@@ -1394,8 +1433,8 @@ struct Scratch {
 };
 template <class T>
 static T* scratch(int slot, size_t count) {
-    static thread_local Scratch slots[16];
-    Scratch& sl = slots[slot];
+    static thread_local Scratch slots[kMaxDevices][16];
+    Scratch& sl = slots[cur_dev()][slot];
     const size_t want = count * sizeof(T) + 64;
     if (want > sl.bytes) {
         if (sl.p) {
@@ -1455,7 +1494,11 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         UA_CK(cudaMemsetAsync(mark.p, 0, sizeof(int) * n, s));
         SPtr<int> longs{scratch<int>(13, n)};
         UA_LAUNCH(k_long_rows, std::min(cdiv(n, 256), 4 * 148), 256, 0, s, A, longs.p, ctl.p + 16);
+        DBuf<int> symc(3, s);
+        UA_CK(cudaMemsetAsync(symc.p, 0, 3 * sizeof(int), s));
+        UA_LAUNCH(k_pattern_sym, std::min(cdiv((long long)n * 32, 256), 16 * 148), 256, 0, s, A, symc.p);
         AggCoop g;
+        g.symc = symc.p;
         g.A = A;
         g.longs = longs.p;
         g.nlongs = ctl.p + 16; g.deg = deg; g.seed = seed; g.max_passes = max_passes; g.st = st.p; g.sc = sc.p; g.ms = ms.p;
@@ -1469,7 +1512,8 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
             UA_CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * (4 * 33 + 40), s));
             g.prof = prof.p;
         }
-        static int max_blocks = 0;
+        static int max_blocks_dev[kMaxDevices] = {};
+        int& max_blocks = max_blocks_dev[cur_dev()];
         if (!max_blocks) {
             int per_sm = 0, dev = 0, sms = 0;
             UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aggregate_coop, 256, 0));
@@ -1486,7 +1530,8 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
         if (n <= cl_max && !no_cluster) {
             // small level: every pass is a chain of latency-bound phases;
             // one 16-CTA cluster with hardware barriers instead of the grid
-            static bool attr = false;
+            static bool attr_dev[kMaxDevices] = {};
+            bool& attr = attr_dev[cur_dev()];
             if (!attr) {
                 UA_CK(cudaFuncSetAttribute(k_aggregate_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 attr = true;

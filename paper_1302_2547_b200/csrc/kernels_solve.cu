@@ -141,7 +141,8 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
     BodyFcgUpd u{};
     u.step = step; u.x = x; u.p = p; u.rin = r; u.rout = r_out; u.ap = ap; u.st = st; u.singular = 0;
     u.red = {rs.partials, rs.ticket};
-    static int maxg = 0;
+    static int maxg_dev[kMaxDevices] = {};
+    int& maxg = maxg_dev[cur_dev()];
     if (!maxg) {
         int occ = 0;
         UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dir_update<SrcDir>, 32 * kGrpWarps, 0));
@@ -448,6 +449,25 @@ __global__ void k_dense_solve(int n, const double* __restrict__ M, const double*
 void launch_dense_solve(int n, const double* Minv, const double* b, double* x, const int* gate, Exec ex) {
     if (n == 0) return;
     UA_LAUNCH_PDL(k_dense_solve, cdiv(n, 8), 256, 0, ex.s, n, Minv, b, x, gate);
+}
+
+// x = M b for nrhs right-hand sides (row-major n x nrhs): warp per output,
+// the same lane-strided dot + shuffle tree as k_dense_solve, so nrhs = 1
+// gives the solve path's bits
+__global__ void k_dense_apply(int n, const double* __restrict__ M, const double* __restrict__ b, int nrhs,
+                              double* x) {
+    const int lane = threadIdx.x & 31;
+    const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= (long long)n * nrhs) return;
+    const int row = (int)(w / nrhs), c = (int)(w % nrhs);
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc += M[(size_t)row * n + j] * b[(size_t)j * nrhs + c];
+    acc = warp_sum(acc);
+    if (lane == 0) x[(size_t)row * nrhs + c] = acc;
+}
+void launch_dense_apply(int n, const double* Minv, const double* b, int nrhs, double* x, cudaStream_t s) {
+    if (n == 0 || nrhs == 0) return;
+    UA_LAUNCH(k_dense_apply, cdiv((long long)n * nrhs, 8), 256, 0, s, n, Minv, b, nrhs, x);
 }
 
 void launch_norm(int n, const double* v, double* out, RedScratch rs, cudaStream_t s) {

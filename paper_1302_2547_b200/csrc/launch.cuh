@@ -53,7 +53,19 @@ inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi&
     }
     if (G.tma_cap > 0 && G.np == 0) {
         // large level: TMA-pipelined persistent tiles
-        static int occ = -1, smem_set = 0;
+        static int occ_dev[kMaxDevices], smem_set_dev[kMaxDevices];
+        static size_t occ_smem_dev[kMaxDevices];
+        static bool init_dev[kMaxDevices];
+        const int dev = cur_dev();
+        if (!init_dev[dev]) {
+            occ_dev[dev] = -1;
+            smem_set_dev[dev] = 0;
+            occ_smem_dev[dev] = 0;
+            init_dev[dev] = true;
+        }
+        int& occ = occ_dev[dev];
+        int& smem_set = smem_set_dev[dev];
+        size_t& occ_smem = occ_smem_dev[dev];
         const size_t smem = tma_smem_bytes(G.tma_cap);
         auto kfn = k_csr_tma<Src, Epi, Unit>;
         if ((int)smem > smem_set) {
@@ -61,7 +73,6 @@ inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi&
             smem_set = (int)smem;
             occ = -1;
         }
-        static size_t occ_smem = 0;
         if (occ < 0 || occ_smem != smem) {
             UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem));
             occ_smem = smem;

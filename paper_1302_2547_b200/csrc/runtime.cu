@@ -182,7 +182,9 @@ cudaStream_t library_stream() {
 static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
                                    const uaamg_setup_params& P, cudaStream_t s) {
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
-    static bool pool_configured = false;
+    const int dev_ = cur_dev();
+    static bool pool_configured_dev[kMaxDevices] = {};
+    bool& pool_configured = pool_configured_dev[dev_];
     if (!pool_configured) {
         // keep freed blocks in the stream-ordered pool: setup allocates and
         // frees O(nnz) scratch per level; returning it to the driver on every
@@ -199,7 +201,8 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         // pre-grow the pool to this setup's transient peak (Galerkin hash +
         // aggregation scratch ~ 40 B/nonzero + 64 B/row) in one block, so the
         // level-0 scratch never waits on a pool growth mid-setup
-        static size_t reserved = 0;
+        static size_t reserved_dev[kMaxDevices] = {};
+        size_t& reserved = reserved_dev[dev_];
         const size_t want = (size_t)40 * (size_t)nnz + (size_t)64 * (size_t)n;
         size_t fr = 0, tot = 0;
         // (cudaMemGetInfo only when the pool would grow: it is a driver query
@@ -337,6 +340,7 @@ namespace {
 std::mutex g_graph_mu;
 struct CachedGraph {
     cudaGraphExec_t e;
+    int dev;
     int par;
     size_t nodes;
 };
@@ -344,9 +348,10 @@ std::vector<CachedGraph> g_graph_cache;
 constexpr size_t kGraphCacheMax = 8;
 }  // namespace
 cudaGraphExec_t graph_cache_take(int par, size_t nodes) {
+    const int dev = cur_dev();
     std::lock_guard<std::mutex> lk(g_graph_mu);
     for (size_t k = g_graph_cache.size(); k-- > 0;) {
-        if (g_graph_cache[k].par == par && g_graph_cache[k].nodes == nodes) {
+        if (g_graph_cache[k].dev == dev && g_graph_cache[k].par == par && g_graph_cache[k].nodes == nodes) {
             cudaGraphExec_t e = g_graph_cache[k].e;
             g_graph_cache.erase(g_graph_cache.begin() + k);
             return e;
@@ -354,14 +359,14 @@ cudaGraphExec_t graph_cache_take(int par, size_t nodes) {
     }
     return nullptr;
 }
-void graph_cache_give(cudaGraphExec_t e, int par, size_t nodes) {
+void graph_cache_give(cudaGraphExec_t e, int dev, int par, size_t nodes) {
     if (!e) return;
     std::lock_guard<std::mutex> lk(g_graph_mu);
     if (g_graph_cache.size() >= kGraphCacheMax) {  // evict the oldest
         cudaGraphExecDestroy(g_graph_cache.front().e);
         g_graph_cache.erase(g_graph_cache.begin());
     }
-    g_graph_cache.push_back({e, par, nodes});
+    g_graph_cache.push_back({e, dev, par, nodes});
 }
 
 int mapped_slot_acquire(int** host, int** dev) {
@@ -387,6 +392,7 @@ void mapped_slot_release(int k) {
 std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels) {
     std::unique_ptr<SolveWs> ws(new SolveWs());
     ws->key = p;
+    ws->dev = cur_dev();
     static const bool wsprof = getenv("UAAMG_WS_PROF") != nullptr;  // diagnostics
     double wlast = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     auto wmark = [&](const char* what) {
@@ -800,6 +806,35 @@ int uaamg_hierarchy_level(const uaamg_hierarchy* h, int level, uaamg_level_view*
         v->coarse_vertex_of_agg = L.nc ? L.seeds.p : nullptr;
         v->agg_ptr = L.nc ? L.agg_ptr.p : nullptr;
         v->members = L.nc ? L.members.p : nullptr;
+    })
+}
+
+int uaamg_hierarchy_coarse(const uaamg_hierarchy* h, const double** minv, int* n, int* mode) {
+    UA_GUARD({
+        *minv = h->Minv.p;
+        *n = h->levels.back()->n;
+        *mode = h->coarse_mode;
+    })
+}
+
+int uaamg_coarse_factor(int n, int64_t nnz, const int* row_ptr, const int* col, const double* val, int singular,
+                        double* minv, int* mode, void* stream) {
+    UA_GUARD({
+        if (n < 0) throw Error(UAAMG_EINVAL, "negative size");
+        Csr A;
+        A.n = n; A.nnz = (int)nnz; A.rp = row_ptr; A.ci = col; A.av = val;
+        cudaStream_t s = (cudaStream_t)stream;
+        DBuf<double> M;
+        *mode = device_coarse_factor(A, singular != 0, M, s);
+        if (n) UA_CK(cudaMemcpyAsync(minv, M.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+        UA_CK(cudaStreamSynchronize(s));
+    })
+}
+
+int uaamg_dense_apply(int n, const double* minv, const double* b, int nrhs, double* x, void* stream) {
+    UA_GUARD({
+        if (n < 0 || nrhs < 0) throw Error(UAAMG_EINVAL, "negative size");
+        launch_dense_apply(n, minv, b, nrhs, x, (cudaStream_t)stream);
     })
 }
 

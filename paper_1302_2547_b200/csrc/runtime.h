@@ -52,10 +52,11 @@ void mapped_slot_release(int k);
 // tried on a graph of the same shape, so it does not fail into a fresh
 // instantiation (several ms) inside a timed solve
 cudaGraphExec_t graph_cache_take(int par, size_t nodes);
-void graph_cache_give(cudaGraphExec_t e, int par, size_t nodes);
+void graph_cache_give(cudaGraphExec_t e, int dev, int par, size_t nodes);
 
 struct SolveWs {
     uaamg_solve_params key{};
+    int dev = 0;            // device the workspace (and its graphs) live on
     bool ready = false;
     std::vector<LevelWs> lev;
     DBuf<FcgState> fcg;     // one per level
@@ -87,7 +88,7 @@ struct SolveWs {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaEvent_t evr[4] = {nullptr, nullptr, nullptr, nullptr};  // lookahead ring (kEvRing)
     ~SolveWs() {
-        for (int k = 0; k < 2; ++k) graph_cache_give(graph[k], k, graph_nodes[k]);  // its work has completed
+        for (int k = 0; k < 2; ++k) graph_cache_give(graph[k], dev, k, graph_nodes[k]);  // its work has completed
         for (auto& row : pev)
             for (auto& e : row) if (e) cudaEventDestroy(e);
         mapped_slot_release(flag_slot);

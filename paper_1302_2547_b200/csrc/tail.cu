@@ -843,13 +843,16 @@ bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s) {
     tp.blob.alloc(host.size(), s);
     UA_CK(cudaMemcpyAsync(tp.blob.p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
     UA_CK(cudaStreamSynchronize(s));  // host staging vector is a temporary
-    static bool attr_done = false;
+    const int dev = cur_dev();
+    static bool attr_done_dev[kMaxDevices] = {};
+    bool& attr_done = attr_done_dev[dev];
     if (!attr_done) {
         UA_CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         UA_CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax));
         attr_done = true;
     }
-    static std::map<std::pair<int, int>, bool> fits_cache;  // (cs, smem) -> a cluster can be resident
+    static std::map<std::pair<int, int>, bool> fits_cache_dev[kMaxDevices];  // (cs, smem) -> a cluster fits
+    auto& fits_cache = fits_cache_dev[dev];
     auto fc = fits_cache.find({cs, L.smem_bytes});
     if (fc != fits_cache.end()) {
         if (!fc->second) return false;

@@ -11,14 +11,13 @@ level matrices/aggregations are materialised lazily on attribute access.
 """
 
 import ctypes
-import weakref
 
 import numpy as np
 import torch
 
 from . import _lib
 from .aggregation import Aggregation, AggregationConfig
-from .device import DeviceCSR, cuda_device, ptr, stream, view
+from .device import DeviceCSR, cuda_device, ptr, stream, to_device, to_host, view
 from .sparse import SparseMatrix
 
 
@@ -33,10 +32,6 @@ def galerkin_coarse(a, agg):
     from . import kernel_table
     p, i, v = kernel_table.galerkin_coo(a.indptr, a.indices, a.data, agg.vertex_to_agg, agg.n_coarse)
     return SparseMatrix(agg.n_coarse, agg.n_coarse, p, i, v, _validate=False)
-
-
-class _LazyMatrix:
-    """Host SparseMatrix of a device level, materialised on first use."""
 
 
 class _Native:
@@ -115,18 +110,55 @@ class Level:
 
 
 class CoarseSolver:
-    """Dense factorization of the coarsest operator, held on the device
-    (Cholesky-based inverse, or eigen pseudo-inverse when singular)."""
+    """Dense factorization of the coarsest operator (reference
+    hierarchy.py:31-65), held on the device: ``CoarseSolver(a, singular)``
+    densifies ``a`` (SparseMatrix or DeviceCSR) and stores its Cholesky-based
+    inverse, or -- singular, or Cholesky failed, which then sets
+    ``singular = True`` like the reference -- the eigen pseudo-inverse with
+    the reference's 1e-12 * lambda_max cut (uaamg_coarse_factor).
+    ``solve(b)`` takes one vector or an (n, k) matrix of right-hand-side
+    columns (numpy in -> numpy out, CUDA tensor in -> tensor out)."""
 
-    def __init__(self, h):
-        self._h = weakref.ref(h)  # no cycle through the Hierarchy
-        self.n = h.levels[-1].n
-        self.singular = h.singular
+    def __init__(self, a, singular):
+        self.n = a.n_rows
+        self.singular = bool(singular)
+        self._owner = None
+        if self.n == 0:
+            self._minv = None
+            return
+        d = a if isinstance(a, DeviceCSR) else a.device()
+        self._minv = torch.empty(self.n * self.n, dtype=torch.float64, device=cuda_device())
+        mode = ctypes.c_int()
+        _lib.check(_lib.load().uaamg_coarse_factor(self.n, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val),
+                                                   int(self.singular), ptr(self._minv), ctypes.byref(mode), stream()))
+        self.singular = self.singular or mode.value == 2
+
+    @classmethod
+    def _of_hierarchy(cls, native):
+        """The factor setup() built for the coarsest level.  Holds the
+        native owner (not the Hierarchy), so it stays usable on its own."""
+        self = cls.__new__(cls)
+        minv, n, mode = ctypes.c_void_p(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(_lib.load().uaamg_hierarchy_coarse(native.handle, ctypes.byref(minv), ctypes.byref(n),
+                                                      ctypes.byref(mode)))
+        self.n = n.value
+        self.singular = mode.value == 2
+        self._owner = native
+        self._minv = view(minv.value, self.n * self.n, np.float64, native) if self.n else None
+        return self
 
     def solve(self, b):
-        from .solvers import CycleSpec, Smoother, cycle
-        h = self._h()
-        return cycle(h, CycleSpec(), Smoother(), h.n_levels - 1, b)
+        """Solve against one vector or a matrix of right-hand-side columns."""
+        host = not isinstance(b, torch.Tensor)
+        if self.n == 0:
+            return np.zeros_like(b) if host else torch.zeros_like(b)
+        bd = to_device(b, np.float64)
+        if bd.shape[0] != self.n or bd.dim() not in (1, 2):
+            raise ValueError("coarse right-hand side size mismatch")
+        nrhs = 1 if bd.dim() == 1 else bd.shape[1]
+        x = torch.empty_like(bd)
+        _lib.check(_lib.load().uaamg_dense_apply(self.n, ptr(self._minv), ptr(bd), int(nrhs), ptr(x), stream()))
+        return to_host(x) if host else x
 
 
 class Hierarchy:
@@ -149,7 +181,7 @@ class Hierarchy:
         self.grid_complexity = sum(l.n for l in self.levels) / n0
         self.operator_complexity = sum(l.nnz for l in self.levels) / nnz0
         self.setup_seconds = float(info.setup_seconds)
-        self.coarsest_solver = CoarseSolver(self)
+        self.coarsest_solver = CoarseSolver._of_hierarchy(self._native)
 
     def _level_view(self, l):
         return self._native.level_view(l)

@@ -22,6 +22,7 @@ TEST INFRASTRUCTURE ONLY.
 """
 
 import argparse
+import hashlib
 import os
 import sys
 import time
@@ -46,8 +47,12 @@ CONFIGS = {
 
 
 def input_digests(A):
-    return {"input_sha": np.array(sha(A.indptr, A.indices, A.data)),
-            "input_sha32": np.array(sha(A.indptr.astype(np.int32), A.indices.astype(np.int32), A.data))}
+    h32 = hashlib.sha256()
+    for arr in (A.indptr, A.indices):
+        for k in range(0, arr.shape[0], 1 << 26):  # int32 copies chunk by chunk
+            h32.update(memoryview(arr[k:k + (1 << 26)].astype(np.int32)).cast("B"))
+    h32.update(memoryview(A.data).cast("B"))
+    return {"input_sha": np.array(sha(A.indptr, A.indices, A.data)), "input_sha32": np.array(h32.hexdigest())}
 
 
 def run(key, out_dir, tol=1e-8):
@@ -56,12 +61,14 @@ def run(key, out_dir, tol=1e-8):
     A = build()
     print(f"{name}: n={A.n_rows} nnz={A.nnz} built in {time.perf_counter() - t:.1f}s", flush=True)
     out = input_digests(A)
-    out["n"] = np.array(A.n_rows)
-    out["nnz"] = np.array(A.nnz)
+    ip, ix, a = A.indptr, A.indices, A.data
+    del A  # the oracle keeps its own copy of level 0
+    out["n"] = np.array(ip.shape[0] - 1)
+    out["nnz"] = np.array(ix.shape[0])
     out["threads"] = np.array(O.get_num_threads())
     t = time.perf_counter()
     try:
-        h = O.setup(A.indptr, A.indices, A.data)
+        h = O.setup(ip, ix, a, copy=False)
     except O.OracleError as e:
         out["setup_error"] = np.array(str(e))
         out["setup_seconds"] = np.array(time.perf_counter() - t)
@@ -83,7 +90,7 @@ def run(key, out_dir, tol=1e-8):
         if L.vertex_to_agg is not None:
             out[f"L{l}_v2a_sha"] = np.array(sha(L.vertex_to_agg))
             out[f"L{l}_seeds_sha"] = np.array(sha(L.coarse_vertex_of_agg))
-    del A
+    del ip, ix, a
     b = np.ones(n0)
     t = time.perf_counter()
     x, rep = O.npcg_solve(h, b, tol=tol, max_iters=500)

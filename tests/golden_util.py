@@ -46,7 +46,7 @@ def load(name):
 def sha(*arrays):
     h = hashlib.sha256()
     for a in arrays:
-        h.update(np.ascontiguousarray(a).tobytes())
+        h.update(memoryview(np.ascontiguousarray(a)).cast("B"))
     return h.hexdigest()
 
 

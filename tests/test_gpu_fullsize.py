@@ -1,0 +1,113 @@
+"""BASELINE configs at full size against fixtures made by the oracle port on
+the B200 host (tests/golden/make_oracle_fixtures.py; the oracle is itself
+pinned bit-exact to the reference at every size the reference can run):
+
+* C4  3D 27-point 256^3 (16.8M unknowns, 449M nonzeros),
+* C5  3D 7-point 512^3 (134M unknowns) on one B200,
+* C3  random geometric graph, 2^23 vertices: the largest connected component
+  (solvable) and the literal SURVEY.md 8d graph, whose ~190 isolated
+  vertices make the reference's setup stagnate (same SetupError).
+
+Bar (north star): aggregation maps, seeds and every coarse level's CSR
+(pattern and values) bit-exact; residual history within 1e-10 relative,
+iterations +-1.  Level 0 is the input itself, checked by its digest.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import GOLDEN, assert_history_close, load, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def U():
+    import paper_1302_2547_b200 as U
+    assert torch.cuda.is_available()
+    return U
+
+
+def _have(name):
+    return os.path.exists(os.path.join(GOLDEN, name + ".npz"))
+
+
+def _digest32(d):
+    """SHA-256 of a device CSR in the int32/int32/float64 device layout."""
+    h = hashlib.sha256()
+    for t in (d.row_ptr, d.col, d.val):
+        for k in range(0, t.shape[0], 1 << 26):
+            h.update(memoryview(t[k:k + (1 << 26)].cpu().numpy()).cast("B"))
+    return h.hexdigest()
+
+
+def _check_hierarchy(h, g):
+    assert h.n_levels == int(g["n_levels"]), (h.n_levels, int(g["n_levels"]))
+    assert h.singular == bool(g["singular"])
+    for l, lev in enumerate(h.levels):
+        assert lev.n == int(g[f"L{l}_n"]), f"level {l} size"
+        assert lev.nnz == int(g[f"L{l}_nnz"]), f"level {l} nnz"
+        if l > 0:
+            m = lev.matrix
+            assert sha(m.indptr, m.indices, m.data) == str(g[f"L{l}_csr_sha"]), f"level {l} matrix differs"
+        agg = lev.aggregation
+        if f"L{l}_v2a_sha" in g:
+            assert sha(np.asarray(agg.vertex_to_agg, dtype=np.int64)) == str(g[f"L{l}_v2a_sha"]), f"level {l} v2a"
+            assert sha(np.asarray(agg.coarse_vertex_of_agg, dtype=np.int64)) == str(g[f"L{l}_seeds_sha"]), \
+                f"level {l} seeds"
+    assert abs(h.grid_complexity - float(g["grid_complexity"])) < 1e-12
+    assert abs(h.operator_complexity - float(g["operator_complexity"])) < 1e-12
+
+
+def _solve_and_check(U, h, g):
+    b = torch.ones(h.levels[0].n, dtype=torch.float64, device="cuda")
+    x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500)
+    assert_history_close(rep.residual_history, g, rtol=1e-10)
+    assert rep.iterations == int(g["iterations"])
+    return rep
+
+
+@pytest.mark.parametrize("name,n,stencil", [("oracle_c4_grid3d27_256", 256, 27), ("oracle_c5_grid3d7_512", 512, 7)])
+def test_grid_configs_full_size(U, name, n, stencil):
+    if not _have(name):
+        pytest.skip(f"{name}.npz not generated")
+    from paper_1302_2547_b200 import problems
+    g = load(name)
+    A = problems.grid3d_device(n, stencil)
+    assert A.n_rows == int(g["n"]) and A.nnz == int(g["nnz"])
+    assert _digest32(A) == str(g["input_sha32"]), "device generator differs from the fixture's input"
+    h = U.setup(A)
+    _check_hierarchy(h, g)
+    _solve_and_check(U, h, g)
+
+
+@pytest.fixture(scope="module")
+def rgg_lcc():
+    from paper_1302_2547_b200 import problems
+    return problems.random_geometric(1 << 23, 12.0, 0, largest_component=True)
+
+
+def test_c3_rgg_largest_component_full_size(U, rgg_lcc):
+    g = load("oracle_c3_rgg_lcc_8m")
+    A = rgg_lcc
+    assert sha(A.indptr, A.indices, A.data) == str(g["input_sha"])
+    h = U.setup(A)
+    _check_hierarchy(h, g)
+    _solve_and_check(U, h, g)
+
+
+def test_c3_literal_graph_stagnates_like_the_reference(U):
+    """SURVEY.md 8d's C3 as written: the isolated vertices can never be
+    merged, so setup raises the reference's SetupError at the same level
+    with the same count (the oracle's message)."""
+    from paper_1302_2547_b200 import problems
+    g = load("oracle_c3_rgg_literal_8m")
+    A = problems.random_geometric(1 << 23, 12.0, 0)
+    assert sha(A.indptr, A.indices, A.data) == str(g["input_sha"])
+    with pytest.raises(U.SetupError) as ei:
+        U.setup(A)
+    assert str(ei.value) == str(g["setup_error"])

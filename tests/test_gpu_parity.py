@@ -332,3 +332,22 @@ def test_cycle_bit_reproducible_without_tail(U, level, monkeypatch):
     b = torch.rand(h.levels[level].n, generator=g, dtype=torch.float64).cuda()
     outs = {U.cycle(h, U.CycleSpec(), U.Smoother(), level, b).cpu().numpy().tobytes() for _ in range(4)}
     assert len(outs) == 1
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_aggregate_nonsymmetric_pattern_vs_oracle(U, oracle, seed):
+    """the admission sweeps' neighbour shortcut assumes a
+    structurally symmetric pattern; setup checks the pattern and takes the
+    plain fixpoint otherwise.  A Laplacian with 15% of its upper entries
+    dropped must aggregate exactly like the reference's row-based rule."""
+    from paper_1302_2547_b200 import problems
+    A = problems.grid2d(48)
+    rng = np.random.default_rng(seed)
+    r = np.repeat(np.arange(A.n_rows), np.diff(A.indptr))
+    drop = (A.indices > r) & (rng.random(A.nnz) < 0.15)
+    M = U.SparseMatrix.from_coo(A.n_rows, A.n_rows, r[~drop], A.indices[~drop], A.data[~drop])
+    for cfg in (dict(seed=3), dict(seed=9, max_passes=4)):
+        agg = U.aggregate(M, U.AggregationConfig(**cfg))
+        v2a, seeds = oracle.aggregate(M.indptr, M.indices, M.data, **cfg)
+        assert np.array_equal(agg.vertex_to_agg, v2a)
+        assert np.array_equal(agg.coarse_vertex_of_agg, seeds)
