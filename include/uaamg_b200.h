@@ -211,35 +211,78 @@ typedef struct {
 int uaamg_npcg_solve(uaamg_hierarchy *h, const uaamg_solve_params *p, const double *b, const double *x0, double *x,
                      double *history_host, uaamg_solve_result *res, void *stream);
 
-/* U/solvers.py:190-255 as a ROW-PARTITIONED solve over `nranks` ranks
- * (paper_1302_2547_b200/csrc/shard.cu): levels with at least
- * shard_rows rows (level 0 always) are split into contiguous row ranges, one
- * per rank; smaller levels are replicated.  Halo columns are gathered from
- * the owning rank's buffer inside the SpMV and dot products are folded per
- * rank, then across ranks in rank order.  This build runs the ranks as
- * virtual ranks on the calling device (partition-invariance harness).  Same
- * argument conventions as uaamg_npcg_solve; singular hierarchies are
- * UAAMG_EUNSUPPORTED. */
-int uaamg_npcg_solve_sharded(uaamg_hierarchy *h, const uaamg_solve_params *p, int nranks, int64_t shard_rows,
-                             const double *b, const double *x0, double *x, double *history_host,
-                             uaamg_solve_result *res, void *stream);
+/* ------------------------------------------------------------------ */
+/* Row-partitioned setup and solve over P ranks (
+ * paper_1302_2547_b200/csrc/dist_setup.cu, dist_solve.cu).  Level 0 is split
+ * into P contiguous row blocks; each rank holds and computes only its rows
+ * (global column indices).  Aggregation, renumbering, members and the
+ * Galerkin product run per rank, reading halo entries straight from the
+ * owning rank's memory; coarse levels keep the inherited partition (rank q
+ * owns the aggregates seeded in its rows) until they drop below shard_rows,
+ * then they are gathered and replicated on every rank.  The hierarchy is
+ * bit-identical to uaamg_setup's for any P; solve histories agree within
+ * round-off of the dot products (folded per rank, then in rank order).
+ *
+ * Communicator: rank >= 0 is one process per GPU -- create, then exchange
+ * the 64-byte CUDA IPC handle of every rank's arena (uaamg_comm_handle;
+ * e.g. torch.distributed all_gather), then uaamg_comm_connect with the P
+ * handles in rank order.  rank = -1 runs all P ranks as VIRTUAL ranks in the
+ * calling process on one device (the partition-invariance harness).  Every
+ * buffer a peer reads lives in the rank's arena of arena_bytes. */
+typedef struct uaamg_comm uaamg_comm;
+typedef struct uaamg_dhier uaamg_dhier;
+int uaamg_comm_create(int nranks, int rank, int64_t arena_bytes, uaamg_comm **out);
+int uaamg_comm_handle(uaamg_comm *c, void *handle64);
+int uaamg_comm_connect(uaamg_comm *c, const void *handles);
+int uaamg_comm_barrier(uaamg_comm *c);   /* collective host barrier (teardown) */
+void uaamg_comm_free(uaamg_comm *c);
 
-/* Multi-process form of uaamg_npcg_solve_sharded: one process per GPU,
- * rank `rank` of `nranks`, each with its own (bit-identical) hierarchy.
- * create -> handle (64-byte CUDA IPC handle of this rank's shared-vector
- * arena) -> exchange the handles (e.g. torch.distributed all_gather) ->
- * connect (nranks handles, rank order) -> solve (collective: every rank
- * calls it with the same b / x0) -> free.  Halo columns are read straight
- * from the peers' arenas over NVLink inside the SpMV gathers; phases are
- * separated by a device-side flag barrier; dots are folded in rank order. */
-typedef struct uaamg_dist uaamg_dist;
-int uaamg_dist_create(uaamg_hierarchy *h, const uaamg_solve_params *p, int rank, int nranks, int64_t shard_rows,
-                      uaamg_dist **out);
-int uaamg_dist_handle(uaamg_dist *d, void *handle64);
-int uaamg_dist_connect(uaamg_dist *d, const void *handles);
-int uaamg_dist_solve(uaamg_dist *d, const double *b, const double *x0, double *x, double *history_host,
-                     uaamg_solve_result *res, void *stream);
-void uaamg_dist_free(uaamg_dist *d);
+/* U/hierarchy.py:120-153, collective.  bounds: P+1 level-0 row bounds.
+ * row_ptr/col/val/nnz: one entry per LOCAL rank (1 per process; P for
+ * virtual ranks, in rank order): that rank's rows [bounds[r], bounds[r+1])
+ * as a CSR with local row offsets and global column indices (device).
+ * size_cap must be 0 and passes_per_level 1 (UAAMG_EUNSUPPORTED otherwise).
+ * shard_rows: levels with fewer rows are gathered and replicated. */
+int uaamg_dsetup(uaamg_comm *c, int n, const int *bounds, const int *const *row_ptr, const int *const *col,
+                 const double *const *val, const int64_t *nnz, const uaamg_setup_params *params,
+                 int64_t shard_rows, uaamg_dhier **out, void *stream);
+void uaamg_dhier_free(uaamg_dhier *d);
+
+typedef struct {
+    int n_levels;
+    int n_sharded;          /* levels 0 .. n_sharded-1 are row-partitioned */
+    int singular;
+    double grid_complexity;
+    double operator_complexity;
+    double setup_seconds;
+} uaamg_dhier_info;
+int uaamg_dhier_get_info(const uaamg_dhier *d, uaamg_dhier_info *info);
+
+/* Level l as held by local rank `rank` (device views): a sharded level's
+ * own rows [row_begin, row_end) (local row offsets, global columns), its
+ * v2a (own rows -> global coarse index) and its seeds (own aggregates'
+ * seeds, ascending); a replicated level whole. */
+typedef struct {
+    int n;
+    int64_t nnz;            /* global */
+    int sharded;
+    int row_begin, row_end;
+    int64_t local_nnz;
+    const int *row_ptr;
+    const int *col;
+    const double *val;
+    int n_coarse;           /* global; 0 on the coarsest level */
+    const int *vertex_to_agg;
+    const int *seeds;
+    int n_seeds;
+} uaamg_dlevel_view;
+int uaamg_dhier_level(const uaamg_dhier *d, int level, int rank, uaamg_dlevel_view *view);
+
+/* U/solvers.py:190-255 on a row-partitioned hierarchy, collective.  b, x0
+ * (NULL or one per local rank), x: per local rank, its own rows (device).
+ * Singular hierarchies are UAAMG_EUNSUPPORTED. */
+int uaamg_dsolve(uaamg_dhier *d, const uaamg_solve_params *p, const double *const *b, const double *const *x0,
+                 double *const *x, double *history_host, uaamg_solve_result *res, void *stream);
 
 /* On-device generator of the 3D lattice Laplacians of the benchmark configs
  * (C2/C4/C5), bit-identical to the host builder
@@ -249,6 +292,10 @@ void uaamg_dist_free(uaamg_dist *d);
  * row_ptr (n+1) and returns *nnz; then col/val (nnz each) are filled. */
 int uaamg_gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int *row_ptr, int *col, double *val,
                      int64_t *nnz, void *stream);
+/* rows [row_begin, row_end) only (a rank's block of level 0): local row
+ * offsets, global column indices; same two passes. */
+int uaamg_gen_grid3d_rows(int nx, int ny, int nz, int stencil, int neumann, int row_begin, int row_end,
+                          int *row_ptr, int *col, double *val, int64_t *nnz, void *stream);
 
 /* On-device canonical assembly.
  * uaamg_from_coo: U/sparse.py:56-74 SparseMatrix.from_coo on device
@@ -268,12 +315,13 @@ int uaamg_csr_view(const uaamg_csr *c, int *n_rows, int *n_cols, int64_t *nnz, i
                    double **val);
 void uaamg_csr_free(uaamg_csr *c);
 
-/* Row partitions used by the sharded solve (host-only helpers):
- * level 0 in equal 128-row-aligned contiguous blocks; a coarse level by seed
- * ownership (aggregates are numbered by ascending seed, so rank q owns the
- * aggregates whose seed lies in its fine rows).  bounds: nranks + 1 ints. */
+/* Level-0 row partition of the sharded setup (host-only helper): P equal
+ * 128-row-aligned blocks. */
 int uaamg_partition_rows(int n, int nranks, int *bounds);
-int uaamg_partition_coarse(const int *seeds, int nc, const int *fine_bounds, int nranks, int *bounds);
+/* Coarse-level ranges of the sharded setup's renumbering (host-only):
+ * aggregates are numbered by ascending seed, so rank q's aggregates are
+ * [bounds[q], bounds[q+1]) = exclusive scan of the per-rank seed counts. */
+int uaamg_coarse_bounds(const int64_t *counts, int nranks, int *bounds);
 
 /* Level-0 hot-kernel timing of the last solve run with profile_level0 = 1:
  * device seconds summed over the working iterations (CUDA events captured

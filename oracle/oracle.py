@@ -79,12 +79,20 @@ def lib():
         L.orc_prolongate_add.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp]
         L.orc_smooth_sweeps.argtypes = [ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
+        L.orc_set_select_mode.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
 
 def set_num_threads(n):
     lib().orc_set_num_threads(int(n))
+
+
+def set_select_mode(mode):
+    """0: A^2 pattern unless it would exceed 2^29 entries (then two hops),
+    1: always the A^2 pattern (the reference's formulation), 2: always two
+    maximum hops over A (no A^2)."""
+    lib().orc_set_select_mode(int(mode))
 
 
 def get_num_threads():

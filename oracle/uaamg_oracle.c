@@ -282,6 +282,78 @@ void orc_claim_owners(i64 n, const i64 *p2, const i64 *x2, const double *s, cons
     }
 }
 
+/* The same two functions without forming A^2: the maximum over the
+ * distance-2 neighbourhood as two maximum hops over A (key = (s, -index)).
+ * select: i is a center iff unprocessed and the best unprocessed key within
+ * distance 2 is i's own (or there is none better); claim: the best center
+ * within distance 2, kept iff its score >= s_j (the best key has the best
+ * score, so this equals the pattern loops' filter-then-max).  Identical
+ * results (tests/test_oracle_golden.py checks both modes on every fixture);
+ * used when A^2 would not fit in memory -- C5 (512^3) has coarse levels with
+ * hub rows whose A^2 rows span the whole level. */
+static inline int key_gt(double sa, i64 ia, double sb, i64 ib) { return sa > sb || (sa == sb && ia < ib); }
+static void hop_max(i64 n, const i64 *ip, const i64 *ix, const double *s, const u8 *ok, double *ms, i64 *mi) {
+#pragma omp parallel for schedule(static)
+    for (i64 k = 0; k < n; k++) {
+        double bs = 0.0;
+        i64 bi = -1;
+        for (i64 e = ip[k]; e < ip[k + 1]; e++) {
+            i64 j = ix[e];
+            if (!ok[j]) continue;
+            if (bi < 0 || key_gt(s[j], j, bs, bi)) { bs = s[j]; bi = j; }
+        }
+        ms[k] = bs;
+        mi[k] = bi;
+    }
+}
+static void hop2_best(const i64 *ip, const i64 *ix, const double *ms, const i64 *mi, i64 i, double *bs, i64 *bi) {
+    *bs = 0.0;
+    *bi = -1;
+    for (i64 e = ip[i]; e < ip[i + 1]; e++) {
+        i64 k = ix[e], c = mi[k];
+        if (c < 0) continue;
+        if (*bi < 0 || key_gt(ms[k], c, *bs, *bi)) { *bs = ms[k]; *bi = c; }
+    }
+}
+void orc_select_centers_2hop(i64 n, const i64 *ip, const i64 *ix, const double *s, const u8 *processed, u8 *out) {
+    u8 *ok = (u8 *)malloc((size_t)n);
+    double *ms = (double *)malloc(sizeof(double) * (size_t)n);
+    i64 *mi = (i64 *)malloc(sizeof(i64) * (size_t)n);
+    for (i64 j = 0; j < n; j++) ok[j] = !processed[j];
+    hop_max(n, ip, ix, s, ok, ms, mi);
+#pragma omp parallel for schedule(static)
+    for (i64 i = 0; i < n; i++) {
+        if (processed[i]) { out[i] = 0; continue; }
+        double bs;
+        i64 bi;
+        hop2_best(ip, ix, ms, mi, i, &bs, &bi);
+        out[i] = (u8)(bi < 0 || bi == i || key_gt(s[i], i, bs, bi));
+    }
+    free(ok); free(ms); free(mi);
+}
+void orc_claim_owners_2hop(i64 n, const i64 *ip, const i64 *ix, const double *s, const u8 *processed,
+                           const u8 *is_center, i64 *owner) {
+    double *ms = (double *)malloc(sizeof(double) * (size_t)n);
+    i64 *mi = (i64 *)malloc(sizeof(i64) * (size_t)n);
+    hop_max(n, ip, ix, s, is_center, ms, mi);
+#pragma omp parallel for schedule(static)
+    for (i64 j = 0; j < n; j++) {
+        if (is_center[j]) { owner[j] = j; continue; }
+        owner[j] = -1;
+        if (processed[j]) continue;
+        double bs;
+        i64 bi;
+        hop2_best(ip, ix, ms, mi, j, &bs, &bi);
+        owner[j] = (bi >= 0 && !(bs < s[j])) ? bi : -1;
+    }
+    free(ms); free(mi);
+}
+
+/* 0: A^2 pattern unless it would exceed kA2MaxEntries, 1: always A^2, 2: always two hops */
+static int g_select_mode = 0;
+void orc_set_select_mode(int m) { g_select_mode = m; }
+static const i64 kA2MaxEntries = (i64)1 << 29; /* 4 GB of int64 indices */
+
 /* lower_bound in a sorted i64 range */
 static inline i64 lower_bound(const i64 *v, i64 lo, i64 hi, i64 key) {
     while (lo < hi) {
@@ -403,8 +475,14 @@ i64 orc_aggregate(i64 n, const i64 *ip, const i64 *ix, const double *a, u64 seed
                   i64 cap, i64 *v2a_out, i64 *seeds_out, i64 *pass_centers) {
     if (n <= 0) { set_err("cannot aggregate an empty matrix"); return -1; }
     if (cap <= 0) cap = (i64)1 << 62; /* U/aggregation.py:18,165 */
-    i64 *p2, *x2;
-    orc_squared_pattern(n, ip, ix, &p2, &x2);
+    /* bound on nnz(A^2): sum over rows of the lengths of the rows they reference */
+    i64 bound = 0;
+#pragma omp parallel for reduction(+ : bound) schedule(static)
+    for (i64 i = 0; i < n; i++)
+        for (i64 k = ip[i]; k < ip[i + 1]; k++) bound += ip[ix[k] + 1] - ip[ix[k]];
+    const int two_hop = g_select_mode == 2 || (g_select_mode == 0 && bound > kA2MaxEntries);
+    i64 *p2 = NULL, *x2 = NULL;
+    if (!two_hop) orc_squared_pattern(n, ip, ix, &p2, &x2);
     u8 *processed = (u8 *)calloc((size_t)n, 1);
     u8 *is_center = (u8 *)calloc((size_t)n, 1);
     i64 *v2a = (i64 *)malloc(sizeof(i64) * (size_t)n);
@@ -422,14 +500,16 @@ i64 orc_aggregate(i64 n, const i64 *ip, const i64 *ix, const double *a, u64 seed
         for (i64 i = 0; i < n; i++) left += !processed[i];
         if (left == 0) break;
         orc_scores(n, ip, ix, seed, pass, s);
-        orc_select_centers(n, p2, x2, s, processed, is_center);
+        if (two_hop) orc_select_centers_2hop(n, ip, ix, s, processed, is_center);
+        else orc_select_centers(n, p2, x2, s, processed, is_center);
         i64 nctr = 0;
         for (i64 i = 0; i < n; i++)
             if (is_center[i]) { rank[i] = nctr; centers[nctr++] = i; }
         if (nctr == 0) break;
         if (pass_centers)
             for (i64 b = 0; b < nctr; b++) pass_centers[centers[b]] = pass;
-        orc_claim_owners(n, p2, x2, s, processed, is_center, owner);
+        if (two_hop) orc_claim_owners_2hop(n, ip, ix, s, processed, is_center, owner);
+        else orc_claim_owners(n, p2, x2, s, processed, is_center, owner);
         /* buckets: claimed non-centers grouped by owner rank, ascending j
          * (U/aggregation.py:157-164) */
         memset(bptr, 0, sizeof(i64) * ((size_t)nctr + 1));

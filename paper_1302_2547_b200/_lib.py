@@ -42,6 +42,17 @@ class LevelView(ctypes.Structure):
                 ("vertex_to_agg", _vp), ("coarse_vertex_of_agg", _vp), ("agg_ptr", _vp), ("members", _vp)]
 
 
+class DHierInfo(ctypes.Structure):
+    _fields_ = [("n_levels", _i), ("n_sharded", _i), ("singular", _i), ("grid_complexity", _d),
+                ("operator_complexity", _d), ("setup_seconds", _d)]
+
+
+class DLevelView(ctypes.Structure):
+    _fields_ = [("n", _i), ("nnz", _i64), ("sharded", _i), ("row_begin", _i), ("row_end", _i), ("local_nnz", _i64),
+                ("row_ptr", _vp), ("col", _vp), ("val", _vp), ("n_coarse", _i), ("vertex_to_agg", _vp),
+                ("seeds", _vp), ("n_seeds", _i)]
+
+
 class SolveParams(ctypes.Structure):
     _fields_ = [("kcycle", _i), ("inner_krylov_steps", _i), ("pre_sweeps", _i), ("post_sweeps", _i),
                 ("smoother_l1", _i), ("omega", _d), ("tol", _d), ("max_iters", _i), ("use_graphs", _i),
@@ -83,20 +94,25 @@ _SIGS = {
     "uaamg_dense_apply": (_i, [_i, _vp, _vp, _i, _vp, _vp]),
     "uaamg_npcg_solve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult),
                               _vp]),
-    "uaamg_npcg_solve_sharded": (_i, [_vp, ctypes.POINTER(SolveParams), _i, ctypes.c_int64, _vp, _vp, _vp, _vp,
-                                      ctypes.POINTER(SolveResult), _vp]),
-    "uaamg_dist_create": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _i, ctypes.c_int64, _vp]),
-    "uaamg_dist_handle": (_i, [_vp, _vp]),
-    "uaamg_dist_connect": (_i, [_vp, _vp]),
-    "uaamg_dist_solve": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
-    "uaamg_dist_free": (None, [_vp]),
+    "uaamg_comm_create": (_i, [_i, _i, _i64, ctypes.POINTER(_vp)]),
+    "uaamg_comm_handle": (_i, [_vp, _vp]),
+    "uaamg_comm_connect": (_i, [_vp, _vp]),
+    "uaamg_comm_barrier": (_i, [_vp]),
+    "uaamg_comm_free": (None, [_vp]),
+    "uaamg_dsetup": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(SetupParams), _i64, ctypes.POINTER(_vp),
+                          _vp]),
+    "uaamg_dhier_free": (None, [_vp]),
+    "uaamg_dhier_get_info": (_i, [_vp, ctypes.POINTER(DHierInfo)]),
+    "uaamg_dhier_level": (_i, [_vp, _i, _i, ctypes.POINTER(DLevelView)]),
+    "uaamg_dsolve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
     "uaamg_partition_rows": (_i, [_i, _i, _vp]),
+    "uaamg_coarse_bounds": (_i, [_vp, _i, _vp]),
     "uaamg_gen_grid3d": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "uaamg_gen_grid3d_rows": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "uaamg_from_coo": (_i, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp]),
     "uaamg_assemble_laplacian": (_i, [_i, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp]),
     "uaamg_csr_view": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "uaamg_csr_free": (None, [_vp]),
-    "uaamg_partition_coarse": (_i, [_vp, _i, _vp, _i, _vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_tail_info": (_i, [_vp, _vp, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),
@@ -136,7 +152,13 @@ def check(rc, what=""):
     """Map a UAAMG_E* code to the reference's exception types."""
     if rc == UAAMG_OK:
         return
-    msg = last_error() or what
+    check_code(rc, last_error() or what)
+
+
+def check_code(rc, msg):
+    """check() with the error message already read."""
+    if rc == UAAMG_OK:
+        return
     if rc == UAAMG_EINVAL:
         raise ValueError(msg)
     if rc == UAAMG_ENUMERICAL:

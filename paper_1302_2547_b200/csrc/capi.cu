@@ -47,6 +47,15 @@ int uaamg_gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* row_
     })
 }
 
+int uaamg_gen_grid3d_rows(int nx, int ny, int nz, int stencil, int neumann, int row_begin, int row_end,
+                          int* row_ptr, int* col, double* val, int64_t* nnz, void* stream) {
+    UA_GUARD({
+        const long long r = gen_grid3d(nx, ny, nz, stencil, neumann, row_ptr, col, val, (cudaStream_t)stream,
+                                       row_begin, row_end);
+        if (nnz && r >= 0) *nnz = r;
+    })
+}
+
 int uaamg_k_hash_u01(uint64_t seed, int64_t pass_idx, const int64_t* idx, int64_t m, double* out, void* stream) {
     UA_GUARD(launch_hash_u01(seed, pass_idx, idx, m, out, (cudaStream_t)stream))
 }

@@ -181,7 +181,9 @@ void launch_axpby_init(int n, const double* b, const double* ax, double* r, cuda
 
 // on-device 3D lattice Laplacian: pass 1 (ci == nullptr) writes row_ptr and
 // returns nnz; pass 2 fills col / val
-long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av, cudaStream_t s);
+// (rows [r0, r1) only when r1 >= 0: local row_ptr, global columns)
+long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av, cudaStream_t s,
+                     long long r0 = 0, long long r1 = -1);
 
 // canonical CSR from device triplets (U/sparse.py:56-74) and the graph
 // Laplacian assembly (U/graph.py:63-82); return nnz, allocate the outputs

@@ -275,8 +275,10 @@ __device__ __forceinline__ void inv_diag_fin(int i, double acc, double dii, int 
     if (m <= 0.0) atomicMin(bad_row, i);
     invm[i] = (l1 ? 1.0 : omega) / m;
 }
-__global__ void k_inv_diag(Csr A, int l1, double omega, double* invm, int* bad_row) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+// rows [base, base + n) (a rank's rows of a sharded level: rp and invm are
+// indexed by global row)
+__global__ void k_inv_diag(Csr A, int base, int n, int l1, double omega, double* invm, int* bad_row) {
+    for (int i = base + blockIdx.x * blockDim.x + threadIdx.x; i < base + n; i += gridDim.x * blockDim.x) {
         const int e0 = A.rp[i], e1 = A.rp[i + 1];
         if (e1 - e0 > kSolveLongMin) continue;
         double acc = 0.0, dii = 0.0;
@@ -324,7 +326,7 @@ __global__ void k_inv_diag_long(Csr A, const int4* piece, const int* pbase, int 
 
 void launch_inv_diag(const Csr& A, const GroupBuf& G, int l1, double omega, double* invm, int* bad_row,
                      cudaStream_t s) {
-    UA_LAUNCH(k_inv_diag, map_grid(A.n) * 2, kThreads, 0, s, A, l1, omega, invm, bad_row);
+    UA_LAUNCH(k_inv_diag, map_grid(G.g.n) * 2, kThreads, 0, s, A, G.g.base, G.g.n, l1, omega, invm, bad_row);
     const int nlong = G.pbase.n > 0 ? (int)G.pbase.n - 1 : 0;
     if (nlong > 0 && G.g.long_min == kSolveLongMin)
         UA_LAUNCH(k_inv_diag_long, nlong, kThreads, 0, s, A, G.g.piece, G.g.pbase, l1, omega, invm, bad_row);
@@ -520,22 +522,22 @@ __device__ __forceinline__ int grid_nbrs(int x, int y, int z, int nx, int ny, in
             }
     return k;
 }
-__global__ void k_grid_count(int nx, int ny, int nz, int stencil, int* cnt) {
-    const long long n = (long long)nx * ny * nz;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+// rows [r0, r1) of the lattice; row_ptr / cnt local (index i - r0), columns global
+__global__ void k_grid_count(int nx, int ny, int nz, int stencil, long long r0, long long r1, int* cnt) {
+    for (long long i = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < r1; i += (long long)gridDim.x * blockDim.x) {
         const int z = (int)(i % nz), y = (int)((i / nz) % ny), x = (int)(i / ((long long)ny * nz));
-        cnt[i + 1] = grid_nbrs(x, y, z, nx, ny, nz, stencil, nullptr, (long long)ny * nz, nz);
-        if (i == 0) cnt[0] = 0;
+        cnt[i - r0 + 1] = grid_nbrs(x, y, z, nx, ny, nz, stencil, nullptr, (long long)ny * nz, nz);
+        if (i == r0) cnt[0] = 0;
     }
 }
-__global__ void k_grid_fill(int nx, int ny, int nz, int stencil, int neumann, const int* rp, int* ci, double* av) {
-    const long long n = (long long)nx * ny * nz;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+__global__ void k_grid_fill(int nx, int ny, int nz, int stencil, int neumann, long long r0, long long r1, const int* rp,
+                            int* ci, double* av) {
+    for (long long i = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < r1; i += (long long)gridDim.x * blockDim.x) {
         const int z = (int)(i % nz), y = (int)((i / nz) % ny), x = (int)(i / ((long long)ny * nz));
         int off[27];
         const int k = grid_nbrs(x, y, z, nx, ny, nz, stencil, off, (long long)ny * nz, nz);
         const double diag = neumann ? (double)(k - 1) : (double)(stencil - 1);
-        int p = rp[i];
+        int p = rp[i - r0];
         for (int q = 0; q < k; ++q, ++p) {
             ci[p] = (int)(i + off[q]);
             av[p] = off[q] == 0 ? diag : -1.0;
@@ -545,14 +547,21 @@ __global__ void k_grid_fill(int nx, int ny, int nz, int stencil, int neumann, co
 }  // namespace
 
 long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, int* ci, double* av,
-                     cudaStream_t s) {
-    const long long n = (long long)nx * ny * nz;
-    if (n <= 0 || n > 0x7fffffffll) throw Error(UAAMG_EINVAL, "grid size out of range");
+                     cudaStream_t s, long long r0, long long r1) {
+    const long long N = (long long)nx * ny * nz;
+    if (N <= 0 || N > 0x7fffffffll) throw Error(UAAMG_EINVAL, "grid size out of range");
     if (stencil != 7 && stencil != 27) throw Error(UAAMG_EINVAL, "stencil must be 7 or 27");
-    const int grid = std::min(cdiv(n, 256), 8 * kNumSMs);
+    if (r1 < 0) r1 = N;
+    if (r0 < 0 || r0 > r1 || r1 > N) throw Error(UAAMG_EINVAL, "row range out of the grid");
+    const long long n = r1 - r0;
+    const int grid = std::max(1, std::min(cdiv(n, 256), 8 * kNumSMs));
     if (!ci) {
         // pass 1: row_ptr (counts + inclusive scan), returns nnz
-        UA_LAUNCH(k_grid_count, grid, 256, 0, s, nx, ny, nz, stencil, rp);
+        if (n == 0) {
+            UA_CK(cudaMemsetAsync(rp, 0, sizeof(int), s));
+            return 0;
+        }
+        UA_LAUNCH(k_grid_count, grid, 256, 0, s, nx, ny, nz, stencil, r0, r1, rp);
         size_t tmp = 0;
         UA_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, rp + 1, rp + 1, (int)n, s));
         DBuf<char> t(tmp, s);
@@ -562,7 +571,7 @@ long long gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* rp, 
         UA_CK(cudaStreamSynchronize(s));
         return nnz;
     }
-    UA_LAUNCH(k_grid_fill, grid, 256, 0, s, nx, ny, nz, stencil, neumann, rp, ci, av);
+    if (n) UA_LAUNCH(k_grid_fill, grid, 256, 0, s, nx, ny, nz, stencil, neumann, r0, r1, rp, ci, av);
     return -1;
 }
 }  // namespace uaamg

@@ -179,8 +179,10 @@ cudaStream_t library_stream() {
     return st;
 }
 
-static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
-                                   const uaamg_setup_params& P, cudaStream_t s) {
+// level_offset: index of this matrix's level in a larger hierarchy (the
+// replicated coarse part of a sharded setup), for error messages
+uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
+                            const uaamg_setup_params& P, cudaStream_t s, int level_offset) {
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
     const int dev_ = cur_dev();
     static bool pool_configured_dev[kMaxDevices] = {};
@@ -270,7 +272,8 @@ static uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const in
         aggregate_level(*cur, P, s);
         mark(lt + "aggregate");
         if (cur->nc == cur->n)
-            throw Error(UAAMG_ESETUP, "aggregation stagnated at level " + std::to_string(h->levels.size()) + ": " +
+            throw Error(UAAMG_ESETUP, "aggregation stagnated at level " +
+                                          std::to_string(level_offset + (int)h->levels.size()) + ": " +
                                           std::to_string(cur->n) + " vertices produced no coarsening");
         cur->agg_ptr.alloc(cur->nc + 1, s);
         cur->members.alloc(cur->n, s);
@@ -773,7 +776,7 @@ int uaamg_setup(int n, int64_t nnz, const int* row_ptr, const int* col, const do
         if (params->passes_per_level != 1 && params->passes_per_level != 2)
             throw Error(UAAMG_EAGG, "passes_per_level must be 1 or 2");
         if (params->max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
-        *out = setup_impl(n, nnz, row_ptr, col, val, *params, (cudaStream_t)stream);
+        *out = setup_impl(n, nnz, row_ptr, col, val, *params, (cudaStream_t)stream, 0);
     })
 }
 

@@ -141,8 +141,7 @@ def cycle(h, spec, smoother, level, b):
     return to_host(x) if host else x
 
 
-def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use_graphs=True,
-               ranks=None, shard_rows=262144):
+def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use_graphs=True):
     """Flexible PCG with one K-/V-cycle per application, on the device."""
     if tol <= 0:
         raise ValueError("tol must be positive")
@@ -155,15 +154,8 @@ def npcg_solve(h, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use
     hist = np.zeros(int(max_iters) + 1)
     P = _params(cycle_spec, smoother, tol, max_iters, use_graphs)
     res = _lib.SolveResult()
-    if ranks is None:
-        rc = _lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), ptr(bd), ptr(x0d), ptr(x),
-                                          hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res), stream())
-    else:
-        # row-partitioned solve over `ranks` virtual ranks (shard.cu): levels
-        # with >= shard_rows rows sharded by row range, smaller ones replicated
-        rc = _lib.load().uaamg_npcg_solve_sharded(h._handle, ctypes.byref(P), int(ranks), int(shard_rows), ptr(bd),
-                                                  ptr(x0d), ptr(x), hist.ctypes.data_as(ctypes.c_void_p),
-                                                  ctypes.byref(res), stream())
+    rc = _lib.load().uaamg_npcg_solve(h._handle, ctypes.byref(P), ptr(bd), ptr(x0d), ptr(x),
+                                      hist.ctypes.data_as(ctypes.c_void_p), ctypes.byref(res), stream())
     report = SolveReport(int(res.iterations), hist[: int(res.iterations) + 1].tolist(), bool(res.converged),
                          {"solve_seconds": float(res.solve_seconds), "setup_seconds": h.setup_seconds})
     if rc == _lib.UAAMG_ENUMERICAL:

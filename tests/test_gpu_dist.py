@@ -1,8 +1,10 @@
-"""Multi-process row-partitioned solve (csrc/shard.cu, uaamg_dist_*): two
-processes share the one GPU of this harness, each with its own hierarchy,
-CUDA-IPC-mapped peer arenas and the device flag barrier between phases.
-The residual history must match the single-process solve within round-off
-(only the dot folds differ) and the reference's within 1e-10."""
+"""Multi-process row-partitioned setup and solve (csrc/dist_setup.cu,
+dist_solve.cu): two processes share the one GPU of this harness, each
+holding only its rows, with CUDA-IPC-mapped peer arenas and the device flag
+barrier between phases -- the code path of one process per GPU on an
+8xB200 box.  Its hierarchy (per-rank blocks) and residual history must be
+bit-identical to the same partition run as virtual ranks in one process,
+and the history within 1e-10 of the reference's."""
 import os
 import socket
 
@@ -23,7 +25,16 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, out):
+def _local_block(ip, ix, a, r0, r1):
+    import torch
+
+    from paper_1302_2547_b200.device import DeviceCSR, to_device_padded
+    e0, e1 = int(ip[r0]), int(ip[r1])
+    return DeviceCSR(r1 - r0, ip.shape[0] - 1, to_device_padded((ip[r0:r1 + 1] - e0).astype(np.int32), np.int32),
+                     to_device_padded(ix[e0:e1].astype(np.int32), np.int32), to_device_padded(a[e0:e1], np.float64))
+
+
+def _worker(rank, world, port, case, shard_rows, out):
     import torch
     import torch.distributed as dist
 
@@ -32,40 +43,59 @@ def _worker(rank, world, port, case, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     import paper_1302_2547_b200 as U
-    from paper_1302_2547_b200.distributed import npcg_solve_distributed
+    from paper_1302_2547_b200 import distributed as D
 
     ip, ix, a, g = problem_for(case)
-    h = U.setup(U.SparseMatrix(ip.shape[0] - 1, ip.shape[0] - 1, ip, ix, a))
-    b = np.ones(ip.shape[0] - 1)
-    x, rep = npcg_solve_distributed(h, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500,
-                                    shard_rows=200)
-    out[rank] = (np.asarray(rep.residual_history).tobytes(), x.tobytes())
+    n = ip.shape[0] - 1
+    bounds = D.partition_rows(n, world)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    dh = D.setup_distributed(_local_block(ip, ix, a, r0, r1), n=n, bounds=bounds, group=dist.group.WORLD,
+                             shard_rows=shard_rows)
+    levels = []
+    for l in range(dh.n_levels):
+        lv = dh.local_level(l)
+        levels.append({k: (v.tobytes() if isinstance(v, np.ndarray) else v) for k, v in lv.items()})
+    b = np.ones(r1 - r0)
+    x, rep = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500)
+    out[rank] = (np.asarray(rep.residual_history).tobytes(), x.tobytes(), levels, dh.n_levels, dh.n_sharded)
+    dh.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["g2d_dir_64"])
-def test_two_process_solve(case):
+@pytest.mark.parametrize("case,shard_rows", [("g2d_dir_64", 200), ("rgg_20000", 1000)])
+def test_two_process_setup_and_solve(case, shard_rows):
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_1302_2547_b200 as U
+    from paper_1302_2547_b200 import distributed as D
 
     ip, ix, a, g = problem_for(case)
-    h = U.setup(U.SparseMatrix(ip.shape[0] - 1, ip.shape[0] - 1, ip, ix, a))
-    x1, r1 = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=float(g["tol"]),
-                          max_iters=500)
+    n = ip.shape[0] - 1
+    A = U.SparseMatrix(n, n, ip, ix, a)
     world = 2
+    dv = D.setup_distributed(A, ranks=world, shard_rows=shard_rows)
+    xv, rv = D.npcg_solve_distributed(dv, U.CycleSpec(), U.Smoother(), np.ones(n), tol=float(g["tol"]), max_iters=500)
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_worker, args=(world, port, case, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, case, shard_rows, out), nprocs=world, join=True)
         res = dict(out)
+    bounds = D.partition_rows(n, world)
     hs = [np.frombuffer(res[r][0]) for r in range(world)]
-    xs = [np.frombuffer(res[r][1]) for r in range(world)]
-    assert np.array_equal(hs[0], hs[1]) and np.array_equal(xs[0], xs[1])
+    assert np.array_equal(hs[0], hs[1])
+    assert np.array_equal(hs[0], np.asarray(rv.residual_history)), "multi-process history differs from virtual ranks"
+    x = np.concatenate([np.frombuffer(res[r][1]) for r in range(world)])
+    assert np.array_equal(x, xv)
     assert_history_close(list(hs[0]), g, rtol=1e-10)
-    h1 = np.asarray(r1.residual_history)
-    assert hs[0].shape == h1.shape
-    assert np.all(np.abs(hs[0] - h1) <= 1e-12 * np.abs(h1) + 1e-15)
-    np.testing.assert_allclose(xs[0], x1, rtol=1e-9, atol=1e-12 * np.abs(x1).max())
+    for r in range(world):
+        assert res[r][3] == dv.n_levels and res[r][4] == dv.n_sharded
+        for l, lv in enumerate(res[r][2]):
+            ref = dv.local_level(l, r if l < dv.n_sharded else 0)
+            for k, v in ref.items():
+                got = lv[k]
+                if isinstance(v, np.ndarray):
+                    assert got == v.tobytes(), f"rank {r} level {l} {k}"
+                else:
+                    assert got == v, f"rank {r} level {l} {k}"

@@ -1,16 +1,18 @@
-"""Row-partitioned (multi-rank) solve, run as P virtual ranks on one GPU
-(paper_1302_2547_b200/csrc/shard.cu).
+"""Row-partitioned setup and solve, run as P virtual ranks on one GPU
+(csrc/dist_setup.cu, csrc/dist_solve.cu).
 
-Partition invariance: for P = 1..8 the residual history must match the
-reference's (golden fixtures) within the solve's 1e-10 bar and the
-single-device solve within round-off -- every SpMV row and restriction sum is
-computed in the same order as on one device; only the dot products are
-folded per rank and then across ranks.
+Partition invariance, the north star's bar:
+* the hierarchy -- aggregation maps, seeds, every coarse level's pattern and
+  values -- is bit-identical to the reference's (golden fixtures) for every
+  rank count, with coarse levels sharded too (small shard_rows);
+* residual histories match the reference's within 1e-10 and the
+  single-device solve within round-off (only the dot products are folded
+  per rank and then across ranks), iterations identical.
 """
 import numpy as np
 import pytest
 
-from golden_util import assert_history_close, problem_for
+from golden_util import assert_hierarchy_equal, assert_history_close, problem_for
 
 pytestmark = pytest.mark.gpu
 
@@ -26,21 +28,45 @@ def U():
     return U
 
 
+@pytest.fixture(scope="module")
+def D():
+    from paper_1302_2547_b200 import distributed as D
+    return D
+
+
 def _smat(U, ip, ix, a):
     return U.SparseMatrix(ip.shape[0] - 1, ip.shape[0] - 1, ip, ix, a)
 
 
-@pytest.mark.parametrize("case", ["c1_grid2d_256", "g3d7_16", "rgg_20000"])
+def _levels(dh):
+    out = []
+    for l in range(dh.n_levels):
+        m = dh.level_matrix(l)
+        ag = dh.level_aggregation(l)
+        out.append(dict(n=m.n_rows, indptr=m.indptr, indices=m.indices, data=m.data,
+                        v2a=None if ag is None else ag[0], seeds=None if ag is None else ag[1]))
+    return out
+
+
+@pytest.mark.parametrize("case", ["c1_grid2d_256", "g3d7_16", "rgg_20000", "wgraph_3000", "g2d_aniso_48"])
 @pytest.mark.parametrize("ranks", [1, 2, 3, 8])
-def test_sharded_history_matches_reference(U, case, ranks):
+def test_sharded_setup_bitexact_and_history(U, D, case, ranks):
+    from golden_util import CASE_CFG
     ip, ix, a, g = problem_for(case)
-    h = U.setup(_smat(U, ip, ix, a))
+    cfg = dict(CASE_CFG.get(case, {}))
+    A = _smat(U, ip, ix, a)
+    # shard every level with >= 200 rows, so coarse levels are sharded too
+    dh = D.setup_distributed(A, ranks=ranks, shard_rows=200, config=U.AggregationConfig(**cfg))
+    assert dh.n_sharded >= 1
+    assert dh.singular == bool(g["singular"])
+    assert_hierarchy_equal(g, _levels(dh))
+    assert abs(dh.grid_complexity - float(g["grid_complexity"])) < 1e-12
+    assert abs(dh.operator_complexity - float(g["operator_complexity"])) < 1e-12
     b = g["b"] if g["b"].shape[0] else np.ones(ip.shape[0] - 1)
     tol = float(g["tol"])
+    h = U.setup(A, U.AggregationConfig(**cfg))
     x1, r1 = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=tol, max_iters=500)
-    # shard every level with >= 1000 rows so coarse levels are sharded too
-    xs, rs = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=tol, max_iters=500, ranks=ranks,
-                          shard_rows=1000)
+    xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=tol, max_iters=500)
     assert_history_close(rs.residual_history, g, rtol=1e-10)
     assert rs.iterations == r1.iterations
     h1 = np.asarray(r1.residual_history)
@@ -50,38 +76,72 @@ def test_sharded_history_matches_reference(U, case, ranks):
 
 
 @pytest.mark.parametrize("kw", [{"kind": "vcycle"}, {"pre_sweeps": 2, "post_sweeps": 2}, {"inner_krylov_steps": 3},
-                                {"pre_sweeps": 0}])
-def test_sharded_variants_match_single_device(U, kw):
+                                {"pre_sweeps": 0}, {"inner_krylov_steps": 0}])
+def test_sharded_variants_match_single_device(U, D, kw):
     ip, ix, a, g = problem_for("g2d_dir_64")
-    h = U.setup(_smat(U, ip, ix, a))
+    A = _smat(U, ip, ix, a)
+    h = U.setup(A)
+    dh = D.setup_distributed(A, ranks=4, shard_rows=200)
     b = np.ones(ip.shape[0] - 1)
     spec = U.CycleSpec(**kw)
     x1, r1 = U.npcg_solve(h, spec, U.Smoother(), b, tol=1e-10, max_iters=300)
-    xs, rs = U.npcg_solve(h, spec, U.Smoother(), b, tol=1e-10, max_iters=300, ranks=4, shard_rows=200)
+    xs, rs = D.npcg_solve_distributed(dh, spec, U.Smoother(), b, tol=1e-10, max_iters=300)
     assert rs.iterations == r1.iterations
     h1 = np.asarray(r1.residual_history)
     hs = np.asarray(rs.residual_history)
     assert np.all(np.abs(hs - h1) <= 1e-10 * np.abs(h1) + 1e-15)
 
 
-def test_sharded_x0_and_jacobi(U):
+def test_sharded_x0_and_jacobi(U, D):
     ip, ix, a, g = problem_for("g3d7_16")
-    h = U.setup(_smat(U, ip, ix, a))
+    A = _smat(U, ip, ix, a)
+    h = U.setup(A)
+    dh = D.setup_distributed(A, ranks=5, shard_rows=100)
     n = ip.shape[0] - 1
     rng = np.random.default_rng(3)
     b = rng.standard_normal(n)
     x0 = rng.standard_normal(n)
     sm = U.Smoother(kind="jacobi")
     x1, r1 = U.npcg_solve(h, U.CycleSpec(), sm, b, tol=1e-9, max_iters=200, x0=x0)
-    xs, rs = U.npcg_solve(h, U.CycleSpec(), sm, b, tol=1e-9, max_iters=200, x0=x0, ranks=5, shard_rows=100)
+    xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), sm, b, tol=1e-9, max_iters=200, x0=x0)
     assert rs.iterations == r1.iterations
     np.testing.assert_allclose(rs.residual_history, r1.residual_history, rtol=1e-10, atol=1e-15)
 
 
-def test_sharded_c2_full_size(U):
-    """C2 (128^3): levels 0 and 1 sharded over 8 ranks, the rest replicated."""
-    ip, ix, a, g = problem_for("c2_grid3d7_128")
-    h = U.setup(_smat(U, ip, ix, a))
+def test_sharded_repeat_is_bit_reproducible(U, D):
+    ip, ix, a, g = problem_for("rgg_20000")
+    dh = D.setup_distributed(_smat(U, ip, ix, a), ranks=3, shard_rows=500)
     b = np.ones(ip.shape[0] - 1)
-    xs, rs = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500, ranks=8)
+    r = [D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=1e-8)[1].residual_history
+         for _ in range(3)]
+    assert r[0] == r[1] == r[2]
+
+
+def test_sharded_c2_full_size(U, D):
+    """C2 (128^3) over 8 ranks with the default shard_rows: levels 0 and 1
+    sharded, the rest replicated; hierarchy SHA-identical to the
+    reference's, history within 1e-10."""
+    ip, ix, a, g = problem_for("c2_grid3d7_128")
+    dh = D.setup_distributed(_smat(U, ip, ix, a), ranks=8)
+    assert dh.n_sharded == 2
+    assert_hierarchy_equal(g, _levels(dh))
+    xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=1e-8,
+                                      max_iters=500)
     assert_history_close(rs.residual_history, g, rtol=1e-10)
+    assert rs.iterations == int(g["iterations"])
+
+
+def test_sharded_errors(U, D):
+    from paper_1302_2547_b200 import problems
+    A = problems.grid2d(32)
+    with pytest.raises(NotImplementedError):
+        D.setup_distributed(A, ranks=2, shard_rows=100, config=U.AggregationConfig(size_cap=4))
+    # stagnation: the reference's SetupError, with the global level index
+    Dg = U.SparseMatrix(400, 400, np.arange(401), np.arange(400), np.full(400, 2.0))
+    with pytest.raises(U.SetupError, match="level 0"):
+        D.setup_distributed(Dg, ranks=2, shard_rows=100)
+    # Neumann hierarchies set up sharded, but the sharded solve refuses them
+    dh = D.setup_distributed(problems.grid2d(32, "neumann"), ranks=2, shard_rows=100)
+    assert dh.singular
+    with pytest.raises(NotImplementedError):
+        D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.zeros(1024))

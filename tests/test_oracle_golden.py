@@ -146,3 +146,17 @@ def test_c2_full_size(oracle):
     assert_hierarchy_equal(g, _oracle_levels(h))
     x, rep = oracle.npcg_solve(h, np.ones(ip.shape[0] - 1), tol=float(g["tol"]), max_iters=500)
     assert_history_close(rep.residual_history, g, rtol=1e-10)
+
+
+@pytest.mark.parametrize("case", HIERARCHY_CASES)
+def test_two_hop_selection_matches_pattern(oracle, case):
+    """The oracle's A^2-free selection/claim (two maximum hops over A, used
+    when A^2 would not fit in memory, e.g. C5's hub levels) gives the
+    reference's hierarchy bit for bit, like the A^2-pattern loops."""
+    ip, ix, a, g = problem_for(case)
+    try:
+        oracle.set_select_mode(2)
+        h = oracle.setup(ip, ix, a, **CASE_CFG.get(case, {}))
+    finally:
+        oracle.set_select_mode(0)
+    assert_hierarchy_equal(g, _oracle_levels(h))
