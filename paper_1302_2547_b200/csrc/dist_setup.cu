@@ -726,7 +726,7 @@ struct Setup {
             const long long E = std::max(ne, 1);
             DBuf<unsigned long long> key(E, s), kalt(E, s);
             DBuf<double> val(E, s), valt(E, s);
-            UA_LAUNCH(kd_gal_emit, std::min(cdiv((long long)Q.n * 32, 256), 16 * kNumSMs), 256, 0, s, Q.n, lptr.p,
+            UA_LAUNCH(kd_gal_emit, std::max(1, std::min(cdiv((long long)Q.n * 32, 256), 16 * kNumSMs)), 256, 0, s, Q.n, lptr.p,
                       R.mem + t0, off.p, L.A, v2a, key.p, val.p);
             // stable sort by (I, J): equal keys keep the reference's order
             cub::DoubleBuffer<unsigned long long> dk(key.p, kalt.p);

@@ -179,7 +179,7 @@ void DistSolve::build() {
         }
         const size_t n0 = std::max(R(0, r).n, 1);
         for (int t = 0; t < kTRoles; ++t) outer[t][r] = C.alloc<double>(r, n0);
-        W.rws = build_ws(H.rep.get(), p, s, 0);
+        W.rws = build_ws(H.rep.get(), p, s, 0, true);
     }
     // the finest level's bad row first (the reference's smooth() order)
     std::vector<long long> bad(P, 0x7fffffff);

@@ -392,7 +392,8 @@ void mapped_slot_release(int k) {
     g_slot_free.push_back(k);
 }
 
-std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels) {
+std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels,
+                                  bool inner0) {
     std::unique_ptr<SolveWs> ws(new SolveWs());
     ws->key = p;
     ws->dev = cur_dev();
@@ -435,14 +436,15 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         LevelWs& W = ws->lev[l];
         const size_t n = std::max(L.n, 1);
         if (sing) W.bp.alloc(n, s);
-        if (l > 0) { W.rhs.alloc(n, s); W.e.alloc(n, s); }
+        const bool inner = l > 0 || inner0;  // reached by restriction (has its own rhs / correction)
+        if (inner) { W.rhs.alloc(n, s); W.e.alloc(n, s); }
         if (l == nl - 1) continue;
         W.invm.alloc(n, s);
         W.r.alloc(n, s);
         W.tA.alloc(n, s);
         W.tB.alloc(n, s);
         if ((L.n >= kTmaMinRows || l < mat_levels) && p.post_sweeps > 1) W.xup.alloc(n, s);
-        if (l > 0 && p.kcycle && p.inner_krylov_steps > 0) {
+        if (inner && p.kcycle && p.inner_krylov_steps > 0) {
             W.xf.alloc(n, s); W.rf.alloc(n, s); W.z.alloc(n, s);
             W.p0.alloc(n, s); W.p1.alloc(n, s); W.ap0.alloc(n, s); W.ap1.alloc(n, s);
         }

@@ -341,7 +341,9 @@ struct Plan {
 void ensure_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s);
 cudaStream_t library_stream();
 // a fresh solve workspace; levels < mat_levels materialise the
-// pre-smoothed / prolongated iterates
-std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels);
+// pre-smoothed / prolongated iterates; inner0: level 0 is itself reached by
+// restriction (the replicated part of a sharded hierarchy)
+std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels,
+                                  bool inner0 = false);
 
 }  // namespace uaamg
