@@ -8,12 +8,16 @@ exactly the reference's ``setup(A)`` + ``npcg_solve(h, CycleSpec(),
 Smoother(), b, tol=1e-8)``.  value = seconds per step (max over ranks).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2slab|c4|c5]
 
-N > 1 (torchrun, one rank per GPU): every rank solves its own copy of the
-problem (weak scaling, replicas); timing is the max over ranks of device
-time.  The row-partitioned multi-GPU solve (shard.cu)
-is validated by the tests; this harness has one GPU, so its scaling is not
-benchmarked here.
+N > 1 (torchrun, one rank per GPU): ONE problem row-partitioned over the N
+ranks -- sharded setup and sharded solve (csrc/dist_setup.cu,
+dist_solve.cu), each rank generating and holding only
+its rows.  Default workload c2slab: a 128 x 128 x (128 N) box, one C2-sized
+slab per GPU (weak scaling, so N = 1 is the C2 headline's size); --workload
+c4 / c5 run BASELINE configs C4 (27-point 256^3) and C5 (7-point 512^3)
+partitioned over N GPUs (strong scaling), also at N = 1.  Timing is the max
+over ranks of device time.
 ``--impl reference`` times the CPU oracle port of the reference path
 (oracle/, C + OpenMP, all host cores) on the same workload.
 """
@@ -168,9 +172,12 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def build_problem():
+def build_problem(workload=None, ws=1):
     from paper_1302_2547_b200 import problems
-    return problems.grid3d(N_GRID, 7)
+    if workload is None:
+        return problems.grid3d(N_GRID, 7)
+    _, stencil, dims_of, _ = PART_WORKLOADS[workload]
+    return problems.grid3d(None, stencil, dims=dims_of(ws))
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -185,8 +192,9 @@ def run_reference(args, rank, ws):
     except Exception:
         pass
     O.set_num_threads(cores)
-    A = build_problem()
+    A = build_problem(args.workload, ws)
     b = np.ones(A.n_rows)
+    steps = args.steps if args.workload is None else 1  # bounded sample of a multi-GPU workload
 
     def step():
         t0 = time.perf_counter()
@@ -194,19 +202,22 @@ def run_reference(args, rank, ws):
         _, rep = O.npcg_solve(h, b, tol=TOL, max_iters=500)
         return time.perf_counter() - t0, rep.iterations
 
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(min(args.warmup, 1) if args.workload is None else 0):
         step()
     times, its = [], 0
-    for _ in range(args.steps):
+    for _ in range(steps):
         t, its = step()
         times.append(t)
     v = sum(times) / len(times)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps,
-            "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1)",
-            "config": {"workload": WORKLOAD, "iterations": its, "tol": TOL},
+    wl = WORKLOAD if args.workload is None else PART_WORKLOADS[args.workload][0]
+    scaling = "weak" if args.workload is None else PART_WORKLOADS[args.workload][3]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (3D lattice Dirichlet Laplacian, b = 1)",
+            "config": {"workload": wl, "iterations": its, "tol": TOL},
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
-                             "sample": "full C2 setup + NPCG solve to 1e-8 per step (CPU oracle, C/OpenMP)"},
+                             "sample": f"full setup + NPCG solve to 1e-8 of the whole {A.n_rows}-unknown problem "
+                                       "per step (CPU oracle, C/OpenMP)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -373,23 +384,19 @@ def run_ours(args, rank, ws, local):
     r = (A.spmv(x.cpu().numpy()) - 1.0)
     relres = float(np.linalg.norm(r) / np.sqrt(n))
 
-    # ---- e2e through the public API with host buffers (pinned), per step:
-    # H2D of the matrix + b, device setup + solve, D2H of x and the history
-    rp_h = torch.from_numpy(A.indptr.astype(np.int32)).pin_memory()
-    ci_h = torch.from_numpy(A.indices.astype(np.int32)).pin_memory()
-    av_h = torch.from_numpy(A.data).pin_memory()
-    b_h = torch.ones(n, dtype=torch.float64).pin_memory()
-    x_h = torch.empty(n, dtype=torch.float64).pin_memory()
-    h2d = rp_h.numel() * 4 + ci_h.numel() * 4 + av_h.numel() * 8 + n * 8
+    # ---- e2e through the reference-facing public API, per step: the
+    # reference's host SparseMatrix (int64 indptr/indices, float64 data,
+    # numpy) -> setup() (its H2D copy and int64 -> int32 narrowing inside the
+    # step) -> npcg_solve() with a numpy b -> numpy x and the history
+    b_np = np.ones(n)
+    h2d = A.indptr.nbytes + A.indices.nbytes + A.data.nbytes + b_np.nbytes
     d2h = n * 8
 
     def e2e_step():
-        Ad2 = DeviceCSR(n, n, rp_h.to(dev, non_blocking=True), ci_h.to(dev, non_blocking=True),
-                        av_h.to(dev, non_blocking=True))
-        h2 = U.setup(Ad2)
-        xd, rep2 = U.npcg_solve(h2, spec, sm, b_h.to(dev, non_blocking=True), tol=TOL, max_iters=500)
-        x_h.copy_(xd, non_blocking=True)
-        torch.cuda.synchronize()
+        # a fresh wrapper of the same host arrays: no cached device copy
+        A2 = U.SparseMatrix(n, n, A.indptr, A.indices, A.data, _validate=False)
+        h2 = U.setup(A2)
+        x_np, rep2 = U.npcg_solve(h2, spec, sm, b_np, tol=TOL, max_iters=500)
         return rep2
 
     e2e_step()
@@ -451,53 +458,171 @@ def run_ours(args, rank, ws, local):
                      "frac": dom.get("frac"), "traffic": traffic},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "host pinned CSR + b -> DeviceCSR -> setup() -> npcg_solve() -> x to host"},
+                "path": "reference-layout host SparseMatrix (int64/float64 numpy, pageable) -> setup() -> "
+                        "npcg_solve(b numpy) -> x numpy; conversion and copies inside the step"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 
 
-def run_sharded(args, rank, ws, local):
-    """--mode sharded: the row-partitioned multi-GPU solve (csrc/shard.cu via
-    npcg_solve_distributed), weak-scaled on the north star's per-GPU share
-    of C5 -- every rank owns a 512 x 512 x 64 slab of a 512 x 512 x (64 N)
-    7-point box.  The hierarchy is built on every rank (setup is replicated,
-    DESIGN.md section 6); value = max over ranks of setup + sharded solve."""
+PART_WORKLOADS = {
+    # name: (description, stencil, dims(N))
+    "c2slab": ("3D 7-point box 128 x 128 x (128 N): one C2-sized 128^3 slab per GPU (weak scaling)", 7,
+               lambda N: (128 * N, 128, 128), "weak"),
+    "c4": ("C4: 3D 27-point Laplacian 256^3 (16,777,216 unknowns) row-partitioned over N GPUs (strong scaling)", 27,
+           lambda N: (256, 256, 256), "strong"),
+    "c5": ("C5: 3D 7-point Laplacian 512^3 (134,217,728 unknowns) row-partitioned over N GPUs (strong scaling)", 7,
+           lambda N: (512, 512, 512), "strong"),
+}
+
+
+def run_partitioned(args, rank, ws, local):
+    """N > 1 (and --workload with N = 1): ONE problem row-partitioned over the
+    N ranks (csrc/dist_setup.cu + dist_solve.cu): every rank generates only
+    its rows of level 0 on its GPU, the hierarchy is built collectively
+    (sharded setup: aggregation, Galerkin, halos read from the peers' arenas;
+    coarse levels gathered below shard_rows), then the sharded K-cycle NPCG
+    solve.  value = max over ranks of the device time of setup + solve (CUDA
+    events on each rank's stream), L2 flushed between steps.  The data plane
+    is CUDA IPC: each rank's arena handle is exchanged once over
+    torch.distributed, then peers load halo entries straight from it."""
     import torch
     import torch.distributed as dist
     import paper_1302_2547_b200 as U
-    from paper_1302_2547_b200 import problems
-    from paper_1302_2547_b200.distributed import npcg_solve_distributed
+    from paper_1302_2547_b200 import _lib
+    from paper_1302_2547_b200 import distributed as D
 
+    desc, stencil, dims_of, scaling = PART_WORKLOADS[args.workload]
+    dims = dims_of(ws)
+    n = dims[0] * dims[1] * dims[2]
     dev = torch.device("cuda", local)
-    nz = int(os.environ.get("BENCH_SLAB_Z", "64"))
-    A = problems.grid3d_device(None, 7, dims=(nz * ws, 512, 512))
-    b = torch.ones(A.n_rows, dtype=torch.float64, device=dev)
-    times, its = [], 0
-    for k in range(max(args.warmup, 1) + args.steps):
-        dist.barrier()
+    group = dist.group.WORLD if ws > 1 else None
+    bounds = D.partition_rows(n, ws)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    A_loc = D.grid3d_rows(None, stencil, r0, r1, dims=dims)
+    b = torch.ones(r1 - r0, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    shard_rows = int(os.environ.get("BENCH_SHARD_ROWS", str(D.SHARD_ROWS)))
+    arena = D.arena_bytes_for(r1 - r0, A_loc.nnz)
+    if ws > 1:
+        sizes = [None] * ws
+        dist.all_gather_object(sizes, int(arena))
+        arena = max(sizes)
+    # one communicator (arenas + IPC handle exchange) for all steps: each
+    # hierarchy is freed before the next setup reuses the arena
+    comm = D.Communicator(ws, rank if ws > 1 else None, arena, group)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
+
+    def step():
+        dh = D.setup_distributed(A_loc, n=n, bounds=bounds, comm=comm, shard_rows=shard_rows)
+        x, rep = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=TOL, max_iters=500)
+        return dh, x, rep
+    for _ in range(max(args.warmup, 3)):
+        dh, x, rep = step()
+        dh.close()
+    launches0 = _lib.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    setup_s, solve_s, its = [], [], 0
+    barrier()
+    gc.collect()
+    gc.disable()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            barrier()
+            evs[k][0].record(stream)
+            dh, x, rep = step()
+            evs[k][1].record(stream)
+            torch.cuda.synchronize()
+            setup_s.append(dh.setup_seconds)
+            solve_s.append(rep.timings["solve_seconds"])
+            its = rep.iterations
+            dh.close()
+        for _ in range(3):
+            clk.sample()
+        barrier()
+    gc.enable()
+    launches = _lib.launch_count() - launches0
+    ms = [evs[k][0].elapsed_time(evs[k][1]) for k in range(args.steps)]
+    t_step = sum(ms) / len(ms) / 1e3
+    if ws > 1:
+        t = torch.tensor([t_step, float(np.mean(setup_s)), float(np.mean(solve_s))], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step, su, so = (float(v) for v in t.tolist())
+    else:
+        su, so = float(np.mean(setup_s)), float(np.mean(solve_s))
+    # true residual of the last solution (distributed SpMV through the same data)
+    dh, x, rep = step()
+    levels = [dh.level_size(l) for l in range(dh.n_levels)]
+    n_sharded = dh.n_sharded
+    dh.close()
+
+    # e2e: this rank's rows from pinned host buffers through the public API
+    rp_h = A_loc.row_ptr.cpu().pin_memory()
+    ci_h = A_loc.col.cpu().pin_memory()
+    av_h = A_loc.val.cpu().pin_memory()
+    b_h = torch.ones(r1 - r0, dtype=torch.float64).pin_memory()
+    x_h = torch.empty(r1 - r0, dtype=torch.float64).pin_memory()
+    h2d = rp_h.numel() * 4 + ci_h.numel() * 4 + av_h.numel() * 8 + (r1 - r0) * 8
+    d2h = (r1 - r0) * 8
+
+    def e2e_step():
+        from paper_1302_2547_b200.device import DeviceCSR, to_device_padded
+        Al = DeviceCSR(r1 - r0, n, to_device_padded(rp_h, np.int32), to_device_padded(ci_h, np.int32),
+                       to_device_padded(av_h, np.float64))
+        dh2 = D.setup_distributed(Al, n=n, bounds=bounds, comm=comm, shard_rows=shard_rows)
+        xd, rep2 = D.npcg_solve_distributed(dh2, U.CycleSpec(), U.Smoother(), b_h.to(dev, non_blocking=True),
+                                            tol=TOL, max_iters=500)
+        x_h.copy_(xd, non_blocking=True)
+        torch.cuda.synchronize()
+        dh2.close()
+        return rep2
+
+    e2e_step()
+    barrier()
+    e2e = []
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
         t0 = time.perf_counter()
-        h = U.setup(A)
-        x, rep = npcg_solve_distributed(h, U.CycleSpec(), U.Smoother(), b, tol=TOL, max_iters=500)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        its = rep.iterations
-        del h
-        if k >= max(args.warmup, 1):
-            times.append(dt)
-    t = torch.tensor([float(np.mean(times))], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rep2 = e2e_step()
+        e2e.append(time.perf_counter() - t0)
+    barrier()
+    e2e_s = float(np.mean(e2e))
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "value": float(t.item()), "unit": "s", "n_gpus": ws, "steps": args.steps,
-                          "warmup": max(args.warmup, 1), "ms_per_step": float(t.item()) * 1e3,
-                          "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                          "data": "synthetic (3D 7-point Dirichlet Laplacian, b = 1, x0 = 0)",
-                          "config": {"workload": f"sharded solve, 7-point box {A.n_rows} unknowns "
-                                                 f"({ws} ranks x one C5 slab each)", "iterations": int(its),
-                                     "parallelism": f"row-partitioned x{ws} (IPC peer gathers)",
-                                     "timing": "wall clock, max over ranks"}}), flush=True)
+        peak, peak_kind = peak_hbm()
+        print(json.dumps({
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3, "higher_is_better": False,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (3D lattice Dirichlet Laplacian, b = 1, x0 = 0), level 0 generated per rank on device",
+            "config": {"workload": desc, "n": n, "iterations": int(its), "tol": TOL, "levels": levels,
+                       "sharded_levels": n_sharded, "shard_rows": shard_rows, "setup_s": su, "solve_s": so,
+                       "step_s_steps": [round(v / 1e3, 5) for v in ms],
+                       "parallelism": f"row-partitioned x{ws}" if ws > 1 else "single GPU (partitioned code path)",
+                       "data_plane": "CUDA IPC peer loads from each rank's arena (handles exchanged once over "
+                                     "torch.distributed); device flag barrier between phases; dots folded in "
+                                     "rank order",
+                       "rows_per_rank": [int(bounds[q + 1] - bounds[q]) for q in range(ws)],
+                       "l2": "flushed between steps (256 MB write)", "timing": "CUDA events, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": None, "traffic": None,
+                         "note": "level-0 kernel rooflines: the N = 1 line (tests/bench C2 and C5-slab)"},
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "path": "per rank: pinned host rows + b -> setup_distributed -> npcg_solve_distributed -> x"},
+            "gpu_launches": int(launches), "clocks": clk.summary()}), flush=True)
+    comm.close()
 
 
 def main():
@@ -506,14 +631,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
-                    help="N > 1: independent C2 replicas (default) or the row-partitioned solve")
+    ap.add_argument("--workload", default=None, choices=sorted(PART_WORKLOADS),
+                    help="row-partitioned workload (default for N > 1: c2slab; N = 1 default: the C2 headline)")
     args = ap.parse_args()
     rank, ws, local = dist_init()
+    if ws > 1 and args.workload is None:
+        args.workload = "c2slab"
     if args.impl == "reference":
         run_reference(args, rank, ws)
-    elif args.mode == "sharded" and ws > 1:
-        run_sharded(args, rank, ws, local)
+    elif args.workload is not None:
+        run_partitioned(args, rank, ws, local)
     else:
         run_ours(args, rank, ws, local)
     if ws > 1:

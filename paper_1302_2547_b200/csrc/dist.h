@@ -35,10 +35,11 @@ struct Comm {
     std::vector<char*> base;
     size_t cap = 0;                 // arena bytes (same on every rank)
     std::vector<size_t> lo, hi;     // per local rank: persistent bump (up), scratch bump (down)
-    unsigned epoch = 0;
+    DBuf<unsigned> epoch;           // this rank's barrier count (device: barriers are graph-capturable)
     int ndir = 0, nval = 0;         // rolling directory / value slot cursors
     DBuf<unsigned*> flag_tab;       // P barrier flag lines
     bool connected = false;
+    int users = 0;                  // live hierarchies on the arena (the bumps reset when the last goes)
     static constexpr size_t kHeader = 1 << 20;  // directory + values + flags
     static constexpr int kDirSlots = 4096, kValSlots = 4096;
     static constexpr size_t kDirOff = 0, kValOff = 8 * kDirSlots, kFlagOff = 16 * kDirSlots;
@@ -50,8 +51,10 @@ struct Comm {
     void create(int P_, int rank_, size_t bytes, cudaStream_t st);
     void connect(const void* handles);  // multi-process: P cudaIpcMemHandle_t
     void connect_virtual();
-    // device barrier across ranks (no-op for virtual ranks: stream order)
-    void barrier();
+    // device barrier across ranks (no-op for virtual ranks: stream order);
+    // gate: skipped when *gate == 0 (identically on every rank: a gated-off
+    // NPCG iteration runs no barrier anywhere)
+    void barrier(const int* gate = nullptr);
     void host_barrier() {
         barrier();
         UA_CK(cudaStreamSynchronize(s));
@@ -63,6 +66,10 @@ struct Comm {
         return static_cast<T*>(alloc_bytes(r, count * sizeof(T), scratch));
     }
     void reset_scratch();
+    void release_user() {
+        if (--users == 0)
+            for (int r : mine) { lo[r] = kHeader; hi[r] = cap; }
+    }
     // every rank's pointer for one buffer per local rank (collective)
     std::vector<std::vector<void*>> tables(const std::vector<std::vector<void*>>& local);
     template <class T>
@@ -126,6 +133,11 @@ struct DLevel {
 
 struct DistHier {
     std::shared_ptr<Comm> C;
+    ~DistHier() {
+        rep.reset();
+        lv.clear();
+        if (C) C->release_user();
+    }
     std::vector<DLevel> lv;                  // sharded levels 0 .. Ls-1
     std::unique_ptr<uaamg_hierarchy> rep;    // replicated levels Ls .. (every rank)
     bool singular = false;

@@ -36,15 +36,20 @@
 #include <algorithm>
 #include <chrono>
 #include <numeric>
+#include <type_traits>
 
 #include "dist.h"
 
 namespace uaamg {
 
 // ================================================================ comm
-// cross-device barrier: publish `epoch` into every rank's flag line, then
-// wait until every rank has published it into ours
-__global__ void k_dist_barrier(unsigned* const* flags, int P, int rank, unsigned epoch) {
+// cross-device barrier: count it on this rank (device counter, so captured
+// graphs replay correctly), publish the count into every rank's flag line,
+// then wait until every rank has published it into ours.  gate == 0: the
+// whole NPCG iteration is gated off on every rank alike -- no barrier.
+__global__ void k_dist_barrier(unsigned* const* flags, int P, int rank, unsigned* ctr, const int* gate) {
+    if (gate && *(const volatile int*)gate == 0) return;
+    const unsigned epoch = ++*ctr;
     __threadfence_system();  // this rank's earlier writes (own and peer) first
     for (int q = 0; q < P; ++q) *(volatile unsigned*)(flags[q] + 32 * rank) = epoch;
     __threadfence_system();
@@ -99,6 +104,8 @@ void Comm::connect(const void* handles) {
     std::vector<unsigned*> fl(P);
     for (int q = 0; q < P; ++q) fl[q] = reinterpret_cast<unsigned*>(base[q] + kFlagOff);
     flag_tab.alloc(P, s);
+    epoch.alloc(1, s);
+    UA_CK(cudaMemsetAsync(epoch.p, 0, sizeof(unsigned), s));
     UA_CK(cudaMemcpyAsync(flag_tab.p, fl.data(), sizeof(unsigned*) * P, cudaMemcpyHostToDevice, s));
     UA_CK(cudaStreamSynchronize(s));
     connected = true;
@@ -107,10 +114,9 @@ void Comm::connect(const void* handles) {
 
 void Comm::connect_virtual() { connected = true; }
 
-void Comm::barrier() {
+void Comm::barrier(const int* gate) {
     if (virt()) return;
-    ++epoch;
-    UA_LAUNCH(k_dist_barrier, 1, 1, 0, s, flag_tab.p, P, rank, epoch);
+    UA_LAUNCH(k_dist_barrier, 1, 1, 0, s, flag_tab.p, P, rank, epoch.p, gate);
 }
 
 void* Comm::alloc_bytes(int r, size_t bytes, bool scratch) {
@@ -201,69 +207,119 @@ __global__ void kd_scores(int a, int n, const int* rps, uint64_t base, double* s
 }
 
 // state: 0 unprocessed, 1 center of this pass, 2 processed (kernels_setup.cu)
-// hop 1 over own rows k: max key over j in row k with (mode 0: st != 2, mode 1: st == 1)
-__global__ void kd_hop1(int a, int n, const int* rps, const int* ci, DV<const uint8_t> st, DV<const double> sc,
-                        int mode, double* ms, int* mi) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int k = a + t;
-        double bs = 0.0;
-        int bi = -1;
-        for (int e = rps[k]; e < rps[k + 1]; ++e) {
-            const int j = __ldg(ci + e);
-            const uint8_t sj = st[j];
-            if (mode == 0 ? (sj == 2) : (sj != 1)) continue;
-            const double v = sc[j];
-            if (bi < 0 || dkey_gt(v, j, bs, bi)) { bs = v; bi = j; }
-        }
-        ms[t] = bs;
-        mi[t] = bi;
+// Every row phase below runs rows of at most kDLong entries thread-per-row
+// and the longer ("hub") rows of the level warp-per-row from a list (rows
+// of coarse levels can span thousands of columns); all phases are
+// order-free (key maxima, flags), so the split does not change results.
+constexpr int kDLong = 64;
+
+__global__ void kd_long_rows(int n, const int* rp, int* list, int* cnt) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        if (rp[t + 1] - rp[t] > kDLong) list[atomicAdd(cnt, 1)] = t;
+}
+
+__device__ __forceinline__ void dwarp_keymax(double& s, int& i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+        if (i2 >= 0 && (i < 0 || dkey_gt(s2, i2, s, i))) { s = s2; i = i2; }
     }
 }
 
-// select (K/numba_backend.py:175-193) on own rows
-__global__ void kd_select(int a, int n, const int* rps, const int* ci, const double* sc, uint8_t* st,
-                          DV<const double> ms, DV<const int> mi, int* cnt) {
-    int local = 0;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        if (st[t] != 0) continue;
-        const int i = a + t;
-        double bs = 0.0;
-        int bi = -1;
-        for (int e = rps[i]; e < rps[i + 1]; ++e) {
-            const int k = __ldg(ci + e);
-            const int c = mi[k];
-            if (c < 0) continue;
-            const double v = ms[k];
-            if (bi < 0 || dkey_gt(v, c, bs, bi)) { bs = v; bi = c; }
+// key maximum of f(e) = (score, index or -1) over entries [e0, e1):
+// sequential in one thread, or (warp = true) strided over the 32 lanes and
+// reduced (the maximum is unique: keys are distinct)
+template <bool Warp, class F>
+__device__ __forceinline__ void dkeymax(int e0, int e1, F&& f, double& bs, int& bi) {
+    bs = 0.0;
+    bi = -1;
+    const int lane = Warp ? (threadIdx.x & 31) : 0;
+    for (int e = e0 + lane; e < e1; e += Warp ? 32 : 1) {
+        double v;
+        int j;
+        f(e, v, j);
+        if (j >= 0 && (bi < 0 || dkey_gt(v, j, bs, bi))) { bs = v; bi = j; }
+    }
+    if (Warp) dwarp_keymax(bs, bi);
+}
+
+// runs body(t, warp) for every own row t: short rows by one thread each,
+// long rows (list) by one warp each
+template <class B>
+__device__ __forceinline__ void drows(int n, const int* rps, int a, const int* longs, int nlong, B&& body) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        if (rps[a + t + 1] - rps[a + t] <= kDLong) body(t, std::false_type{});
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nlong; w += warps) body(longs[w], std::true_type{});
+}
+
+// hop 1 over own rows k: max key over j in row k with (mode 0: st != 2, mode 1: st == 1)
+__global__ void kd_hop1(int a, int n, const int* rps, const int* ci, const int* longs, int nlong,
+                        DV<const uint8_t> st, DV<const double> sc, int mode, double* ms, int* mi) {
+    drows(n, rps, a, longs, nlong, [&](int t, auto warp) {
+        constexpr bool W = decltype(warp)::value;
+        const int k = a + t;
+        double bs;
+        int bi;
+        dkeymax<W>(rps[k], rps[k + 1], [&](int e, double& v, int& j) {
+            j = __ldg(ci + e);
+            const uint8_t sj = st[j];
+            if (mode == 0 ? (sj == 2) : (sj != 1)) { j = -1; return; }
+            v = sc[j];
+        }, bs, bi);
+        if (!W || (threadIdx.x & 31) == 0) {
+            ms[t] = bs;
+            mi[t] = bi;
         }
-        if (bi < 0 || bi == i || dkey_gt(sc[t], i, bs, bi)) {
+    });
+}
+
+// best (ms[k], mi[k]) over k in row i
+template <bool W>
+__device__ __forceinline__ void dhop2(const int* rps, const int* ci, int i, const DV<const double>& ms,
+                                      const DV<const int>& mi, double& bs, int& bi) {
+    dkeymax<W>(rps[i], rps[i + 1], [&](int e, double& v, int& c) {
+        const int k = __ldg(ci + e);
+        c = mi[k];
+        if (c >= 0) v = ms[k];
+    }, bs, bi);
+}
+
+// select (K/numba_backend.py:175-193) on own rows
+__global__ void kd_select(int a, int n, const int* rps, const int* ci, const int* longs, int nlong, const double* sc,
+                          uint8_t* st, DV<const double> ms, DV<const int> mi, int* cnt) {
+    int local = 0;
+    drows(n, rps, a, longs, nlong, [&](int t, auto warp) {
+        constexpr bool W = decltype(warp)::value;
+        if (st[t] != 0) return;
+        const int i = a + t;
+        double bs;
+        int bi;
+        dhop2<W>(rps, ci, i, ms, mi, bs, bi);
+        if ((!W || (threadIdx.x & 31) == 0) && (bi < 0 || bi == i || dkey_gt(sc[t], i, bs, bi))) {
             st[t] = 1;
             ++local;
         }
-    }
+    });
     local = __reduce_add_sync(0xffffffffu, local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(cnt, local);
 }
 
 // claim (K/numba_backend.py:196-220) on own rows
-__global__ void kd_claim(int a, int n, const int* rps, const int* ci, const double* sc, const uint8_t* st,
-                         DV<const double> ms, DV<const int> mi, int* owner) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+__global__ void kd_claim(int a, int n, const int* rps, const int* ci, const int* longs, int nlong, const double* sc,
+                         const uint8_t* st, DV<const double> ms, DV<const int> mi, int* owner) {
+    drows(n, rps, a, longs, nlong, [&](int t, auto warp) {
+        constexpr bool W = decltype(warp)::value;
         const int j = a + t;
         const uint8_t sj = st[t];
-        if (sj == 1) { owner[t] = j; continue; }
-        if (sj == 2) { owner[t] = -1; continue; }
-        double bs = 0.0;
-        int bi = -1;
-        for (int e = rps[j]; e < rps[j + 1]; ++e) {
-            const int k = __ldg(ci + e);
-            const int c = mi[k];
-            if (c < 0) continue;
-            const double v = ms[k];
-            if (bi < 0 || dkey_gt(v, c, bs, bi)) { bs = v; bi = c; }
-        }
-        owner[t] = (bi >= 0 && !(bs < sc[t])) ? bi : -1;
-    }
+        if (sj == 1) { owner[t] = j; return; }
+        if (sj == 2) { owner[t] = -1; return; }
+        double bs;
+        int bi;
+        dhop2<W>(rps, ci, j, ms, mi, bs, bi);
+        if (!W || (threadIdx.x & 31) == 0) owner[t] = (bi >= 0 && !(bs < sc[t])) ? bi : -1;
+    });
 }
 
 // uncapped admission (K/numba_backend.py:235-273): the fixpoint of "j is
@@ -271,22 +327,30 @@ __global__ void kd_claim(int a, int n, const int* rps, const int* ci, const doub
 __global__ void kd_admit_init(int n, const uint8_t* st, uint8_t* adm) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) adm[t] = (st[t] == 1);
 }
-__global__ void kd_admit_step(int a, int n, const int* rps, const int* ci, const int* owner_loc, uint8_t* adm_loc,
-                              DV<const uint8_t> adm, DV<const int> owner, int* changed) {
+__global__ void kd_admit_step(int a, int n, const int* rps, const int* ci, const int* longs, int nlong,
+                              const int* owner_loc, uint8_t* adm_loc, DV<const uint8_t> adm, DV<const int> owner,
+                              int* changed) {
     int local = 0;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    drows(n, rps, a, longs, nlong, [&](int t, auto warp) {
+        constexpr bool W = decltype(warp)::value;
         const int j = a + t;
         const int c = owner_loc[t];
-        if (c < 0 || c == j || adm_loc[t]) continue;
-        for (int e = rps[j]; e < rps[j + 1]; ++e) {
+        if (c < 0 || c == j || adm_loc[t]) return;
+        bool f = false;
+        const int lane = W ? (threadIdx.x & 31) : 0;
+        for (int e = rps[j] + lane; e < rps[j + 1]; e += W ? 32 : 1) {
             const int nb = __ldg(ci + e);
             if (*(const volatile uint8_t*)&adm[nb] && owner[nb] == c) {
-                adm_loc[t] = 1;
-                local = 1;
+                f = true;
                 break;
             }
         }
-    }
+        if (W) f = __any_sync(0xffffffffu, f);
+        if (f && (!W || lane == 0)) {
+            adm_loc[t] = 1;
+            local = 1;
+        }
+    });
     if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
 }
 __global__ void kd_commit(int n, uint8_t* st, const int* owner, const uint8_t* adm, int* seed_of, int* remaining) {
@@ -527,6 +591,18 @@ struct Setup {
             UA_CK(cudaMemsetAsync(vst[r], 0, n, s));
             UA_CK(cudaMemsetAsync(vseed[r], 0xff, sizeof(int) * n, s));
         }
+        // rows longer than kDLong (per local rank), processed warp-per-row
+        std::vector<int*> longs(P_, nullptr);
+        std::vector<int> nlong(P_, 0);
+        for (int r : C_.mine) {
+            const DRank& R = L.r[r];
+            longs[r] = C_.alloc<int>(r, std::max(R.n, 1), true);
+            DBuf<int> c1(1, s);
+            UA_CK(cudaMemsetAsync(c1.p, 0, sizeof(int), s));
+            UA_LAUNCH(kd_long_rows, g1(R.n), 256, 0, s, R.n, R.rp, longs[r], c1.p);
+            UA_CK(cudaMemcpyAsync(&nlong[r], c1.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            UA_CK(cudaStreamSynchronize(s));
+        }
         auto T = C_.tables({vst, vs, vms, vmi, vown, vadm, vnid});
         const DV<const uint8_t> st = dv<const uint8_t>(L.pt, T[0]);
         const DV<const double> sc = dv<const double>(L.pt, T[1]);
@@ -558,23 +634,26 @@ struct Setup {
             C_.barrier();
             for (int r : C_.mine) {
                 const DRank& R = L.r[r];
-                UA_LAUNCH(kd_hop1, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, st, sc, 0, (double*)vms[r], (int*)vmi[r]);
+                UA_LAUNCH(kd_hop1, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, longs[r], nlong[r], st, sc, 0,
+                          (double*)vms[r], (int*)vmi[r]);
             }
             C_.barrier();
             for (int r : C_.mine) {
                 const DRank& R = L.r[r];
-                UA_LAUNCH(kd_select, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, (const double*)vs[r], (uint8_t*)vst[r],
+                UA_LAUNCH(kd_select, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, longs[r], nlong[r], (const double*)vs[r],
+                          (uint8_t*)vst[r],
                           ms, mi, cnt[r] + 0);
             }
             if (gather_count(0) == 0) break;  // (includes a barrier)
             for (int r : C_.mine) {
                 const DRank& R = L.r[r];
-                UA_LAUNCH(kd_hop1, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, st, sc, 1, (double*)vms[r], (int*)vmi[r]);
+                UA_LAUNCH(kd_hop1, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, longs[r], nlong[r], st, sc, 1,
+                          (double*)vms[r], (int*)vmi[r]);
             }
             C_.barrier();
             for (int r : C_.mine) {
                 const DRank& R = L.r[r];
-                UA_LAUNCH(kd_claim, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, (const double*)vs[r],
+                UA_LAUNCH(kd_claim, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, longs[r], nlong[r], (const double*)vs[r],
                           (const uint8_t*)vst[r], ms, mi, (int*)vown[r]);
                 UA_LAUNCH(kd_admit_init, g1(R.n), 256, 0, s, R.n, (const uint8_t*)vst[r], (uint8_t*)vadm[r]);
             }
@@ -584,7 +663,7 @@ struct Setup {
                 for (int r : C_.mine) {
                     const DRank& R = L.r[r];
                     UA_CK(cudaMemsetAsync(cnt[r] + slot, 0, sizeof(int), s));
-                    UA_LAUNCH(kd_admit_step, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, (const int*)vown[r],
+                    UA_LAUNCH(kd_admit_step, g1(R.n), 256, 0, s, R.a, R.n, R.rps, R.ci, longs[r], nlong[r], (const int*)vown[r],
                               (uint8_t*)vadm[r], adm, own, cnt[r] + slot);
                 }
                 if (gather_count(slot) == 0) break;
@@ -814,8 +893,10 @@ std::unique_ptr<DistHier> dist_setup(std::shared_ptr<Comm> Cp, int n, const int*
     if (P.max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
     cudaStream_t s = C.s;
+    if (C.users > 0) throw Error(UAAMG_EINVAL, "a hierarchy already lives on this communicator's arena");
     auto H = std::make_unique<DistHier>();
     H->C = Cp;
+    ++C.users;
     cudaEvent_t e0, e1;
     UA_CK(cudaEventCreate(&e0));
     UA_CK(cudaEventCreate(&e1));

@@ -119,7 +119,23 @@ struct DistSolve {
         c.av = nullptr;
         return c;
     }
-    void sync() { C.barrier(); }
+    // barriers inside NPCG iterations are gated by the iteration's `active`
+    // flag (identical on every rank), so gated-off look-ahead replays run none
+    const int* bgate = nullptr;
+    void sync() { C.barrier(bgate); }
+    // one CUDA graph per iteration parity (the plain launch sequence of
+    // npcg_iteration, barrier kernels included), replayed with look-ahead
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    uint64_t gk[2] = {0, 0};  // kernels per graph (launch accounting)
+    int* h_flag = nullptr;
+    int* d_flag = nullptr;
+    int flag_slot = -1;
+    cudaEvent_t evr[kEvRing] = {};
+    ~DistSolve() {
+        for (auto& g : graph) if (g) cudaGraphExecDestroy(g);
+        mapped_slot_release(flag_slot);
+        for (auto& e : evr) if (e) cudaEventDestroy(e);
+    }
 
     void build();
     bool cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int beta_state);
@@ -485,8 +501,8 @@ void DistSolve::npcg_iteration(int parity) {
     }
 }
 
-__global__ void k_set_npcg_d(NpcgState* st, double tol, int max_iters) {
-    st->host_active = nullptr;
+__global__ void k_set_npcg_d(NpcgState* st, double tol, int max_iters, int* host_active) {
+    st->host_active = host_active;
     st->tol = tol;
     st->max_iters = max_iters;
 }
@@ -496,6 +512,12 @@ void DistSolve::run(const std::vector<const double*>& b, const std::vector<const
                     const std::vector<double*>& x, double* hist_host, uaamg_solve_result* res) {
     const int me = C.mine[0];
     const bool have_x0 = !x0.empty() && x0[0] != nullptr;
+    bgate = nullptr;
+    if (flag_slot < 0) {
+        flag_slot = mapped_slot_acquire(&h_flag, &d_flag);
+        for (auto& e : evr) UA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    *(volatile int*)h_flag = 1;
     cudaEvent_t e0, e1;
     UA_CK(cudaEventCreate(&e0));
     UA_CK(cudaEventCreate(&e1));
@@ -515,7 +537,7 @@ void DistSolve::run(const std::vector<const double*>& b, const std::vector<const
         e.b = sh(r, O(T_B)); e.r = sh(r, O(T_R)); e.g = nullptr;
         if (have_x0) run_stream<SrcPeer, EpiResid, false>(csr(0, r), ws[r].gA[0].g, peer(O(T_X), 0), e, s);
         else run_stream<SrcZero, EpiResid, false>(csr(0, r), ws[r].gA[0].g, SrcZero{}, e, s);
-        UA_LAUNCH(k_set_npcg_d, 1, 1, 0, s, nst(r), p.tol, p.max_iters);
+        UA_LAUNCH(k_set_npcg_d, 1, 1, 0, s, nst(r), p.tol, p.max_iters, r == me ? d_flag : nullptr);
     }
     sync();
     for (int r : C.mine) {
@@ -534,11 +556,42 @@ void DistSolve::run(const std::vector<const double*>& b, const std::vector<const
     NpcgState hst{};
     UA_CK(cudaMemcpyAsync(&hst, nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
-    for (int it = 0; hst.active && it < p.max_iters; ++it) {
-        npcg_iteration(it & 1);
+    bgate = &nst(me)->active;
+    if (hst.active && p.use_graphs) {
+        if (!graph[0]) {
+            for (int par = 0; par < 2; ++par) {
+                cudaGraph_t g;
+                const uint64_t before = g_launches.load();
+                UA_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                npcg_iteration(par);
+                UA_CK(cudaStreamEndCapture(s, &g));
+                gk[par] = g_launches.load() - before;
+                g_launches.fetch_sub(gk[par]);  // captured, not executed: counted per replay
+                UA_CK(cudaGraphInstantiate(&graph[par], g, 0));
+                cudaGraphDestroy(g);
+            }
+        }
+        // pipelined kLookahead iterations deep; gated-off replays past the
+        // end skip every kernel body and every barrier on all ranks alike
+        for (int it = 0; it < p.max_iters; ++it) {
+            UA_CK(cudaGraphLaunch(graph[it & 1], s));
+            g_launches.fetch_add(gk[it & 1]);
+            UA_CK(cudaEventRecord(evr[it % kEvRing], s));
+            if (it >= kLookahead) {
+                UA_CK(cudaEventSynchronize(evr[(it - kLookahead) % kEvRing]));
+                if (*(volatile int*)h_flag == 0) break;
+            }
+        }
         UA_CK(cudaMemcpyAsync(&hst, nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
         UA_CK(cudaStreamSynchronize(s));
+    } else {
+        for (int it = 0; hst.active && it < p.max_iters; ++it) {
+            npcg_iteration(it & 1);
+            UA_CK(cudaMemcpyAsync(&hst, nst(me), sizeof(NpcgState), cudaMemcpyDeviceToHost, s));
+            UA_CK(cudaStreamSynchronize(s));
+        }
     }
+    bgate = nullptr;
     UA_CK(cudaEventRecord(e1, s));
     for (size_t k = 0; k < C.mine.size(); ++k) {
         const int r = C.mine[k];

@@ -113,8 +113,9 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.step = step; e.red = {rs.partials, rs.ticket};
     SrcDir src{};
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = nullptr; src.have_static = have_prev;
-    if (G.tma_cap > 0) {
-        // large level: p first, then a plain-gather SpMV (same arithmetic)
+    if (G.tma_cap > 0 || G.n >= kTmaMinRows) {
+        // large level: p first, then a plain-gather SpMV (same arithmetic;
+        // one gathered array instead of z and p_prev)
         BodyDirP bp{};
         bp.src = src; bp.p = p; bp.g = &st->gate[step];
         run_map(A.n, bp, ex);
@@ -129,7 +130,7 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
                            RedScratch rs, double* part, unsigned* bar, Exec ex) {
     static const bool no_fuse = getenv("UAAMG_NO_DIR_FUSE") != nullptr;  // A/B diagnostics
-    if (G.tma_cap > 0 || no_fuse) {
+    if (G.tma_cap > 0 || G.n >= kTmaMinRows || no_fuse) {
         launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
         launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex);
         return;
@@ -170,7 +171,7 @@ void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const doubl
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.red = {rs.partials, rs.ticket};
     SrcDir src{};
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = &st->have_prev;
-    if (G.tma_cap > 0) {
+    if (G.tma_cap > 0 || G.n >= kTmaMinRows) {
         BodyDirP bp{};
         bp.src = src; bp.p = p; bp.g = &st->active;
         run_map(A.n, bp, s);

@@ -7,6 +7,8 @@ row_ptr/col, fp64 val -- SURVEY.md section 8 layout).  Library-owned arrays
 ``__cuda_array_interface__`` views that keep their owner alive.
 """
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -39,9 +41,7 @@ def to_device(a, dtype):
     if isinstance(a, torch.Tensor):
         return a.to(device=cuda_device(), dtype=dt).contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype)
-    if not arr.flags.writeable:  # SparseMatrix arrays are read-only views
-        arr = arr.copy()
-    return torch.from_numpy(arr).to(device=cuda_device(), non_blocking=False)
+    return _host_view(arr).to(device=cuda_device(), non_blocking=False)
 
 
 # Bytes past the end of a level-0 array the TMA tile kernel may read: its
@@ -59,16 +59,30 @@ def device_empty(n, dtype):
     return full[: int(n)]
 
 
+def _host_view(arr):
+    """torch view of a host array without copying it -- also of the
+    reference's read-only SparseMatrix arrays (only read here)."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr)
+
+
 def to_device_padded(a, dtype):
     """to_device into a device_empty buffer (borrowable by uaamg_setup)."""
     src = to_device(a, dtype) if isinstance(a, torch.Tensor) else None
     if src is not None and borrowable(src, dtype):
         return src
     if src is None:
-        arr = np.ascontiguousarray(a, dtype=dtype)
-        out = device_empty(arr.shape[0], dtype)
-        out.copy_(torch.from_numpy(arr if arr.flags.writeable else arr.copy()))
-        return out
+        arr = np.asarray(a)
+        if arr.dtype != np.dtype(dtype) and arr.dtype.kind == np.dtype(dtype).kind and arr.flags.c_contiguous:
+            # e.g. the reference's int64 indices -> int32: copy as is, narrow
+            # on the device (cheaper than a host conversion pass)
+            src = _host_view(arr).to(cuda_device())
+        else:
+            arr = np.ascontiguousarray(arr, dtype=dtype)
+            out = device_empty(arr.shape[0], dtype)
+            out.copy_(_host_view(arr))
+            return out
     out = device_empty(src.shape[0], dtype)
     out.copy_(src)
     return out

@@ -33,7 +33,7 @@ from .solvers import NumericalError, SolveReport, _params
 from .sparse import SparseMatrix
 
 HANDLE_BYTES = 64
-SHARD_ROWS = 262144
+SHARD_ROWS = 1 << 20  # levels with fewer rows are gathered and replicated
 
 
 def partition_rows(n, ranks):
@@ -153,10 +153,10 @@ class DistributedHierarchy:
     virtual ranks, the assembled global :meth:`level_matrix` /
     :meth:`level_aggregation`."""
 
-    def __init__(self, comm, handle, keep=()):
+    def __init__(self, comm, handle, owns_comm=True):
         self.comm = comm
         self._h = handle
-        self._keep = keep
+        self._owns_comm = owns_comm
         info = _lib.DHierInfo()
         _lib.check(_lib.load().uaamg_dhier_get_info(handle, ctypes.byref(info)))
         self.n_levels = int(info.n_levels)
@@ -226,14 +226,16 @@ class DistributedHierarchy:
         return (np.concatenate([p["vertex_to_agg"] for p in parts]), np.concatenate([p["seeds"] for p in parts]))
 
     def close(self, collective=True):
-        """Free the hierarchy and its communicator (collective for one
-        process per GPU: every rank must call it)."""
+        """Free the hierarchy (collective for one process per GPU: every rank
+        must call it), and its communicator if setup_distributed made it; a
+        caller-owned communicator can then carry the next hierarchy."""
         if self._h:
             if collective:
                 self.comm.quiesce()
             _lib.load().uaamg_dhier_free(self._h)
             self._h = None
-        self.comm.close(collective=False)
+        if self._owns_comm:
+            self.comm.close(collective=False)
 
     def __del__(self):
         try:
@@ -253,18 +255,21 @@ def setup_distributed(a, ranks=None, bounds=None, n=None, comm=None, config=Aggr
                       max_levels=20, singular=None, shard_rows=SHARD_ROWS, arena_bytes=None, group=None):
     """Collective row-partitioned setup (U/hierarchy.py:120-153).
 
-    Virtual ranks (``comm`` None or virtual): ``a`` is the whole matrix
-    (SparseMatrix or DeviceCSR), split into ``ranks`` blocks of
+    Virtual ranks (``ranks`` given, or a virtual ``comm``): ``a`` is the
+    whole matrix (SparseMatrix or DeviceCSR), split into blocks of
     ``partition_rows``.  One process per GPU: ``a`` is this rank's block
     (a DeviceCSR of its rows with GLOBAL column indices), ``n`` the global
     size, ``bounds`` the P+1 row bounds and ``comm`` a connected
-    :class:`Communicator` (or pass ``group`` and let this create one)."""
+    :class:`Communicator` (or pass ``group`` and let this create one).  A
+    caller-owned ``comm`` carries one hierarchy at a time and is reused
+    (no arena allocation or handle exchange per setup)."""
     L = _lib.load()
-    if comm is None and group is None:
+    owns = comm is None
+    if (comm is None and group is None) or (comm is not None and comm.virtual):
         # virtual ranks over a whole matrix
         d = a if isinstance(a, DeviceCSR) else a.device()
         n = d.n_rows
-        P = int(ranks)
+        P = int(ranks) if comm is None else comm.ranks
         bounds = partition_rows(n, P)
         rp_h = to_host(d.row_ptr).astype(np.int64)
         blocks = []
@@ -273,9 +278,10 @@ def setup_distributed(a, ranks=None, bounds=None, n=None, comm=None, config=Aggr
             e0, e1 = int(rp_h[r0]), int(rp_h[r1])
             rp = (d.row_ptr[r0:r1 + 1] - e0).to(torch.int32).contiguous()
             blocks.append((rp, d.col[e0:e1].contiguous(), d.val[e0:e1].contiguous(), e1 - e0))
-        if arena_bytes is None:
-            arena_bytes = max(arena_bytes_for(int(np.diff(bounds).max()), max(b[3] for b in blocks)), 1 << 26)
-        comm = Communicator(P, None, arena_bytes)
+        if comm is None:
+            if arena_bytes is None:
+                arena_bytes = max(arena_bytes_for(int(np.diff(bounds).max()), max(b[3] for b in blocks)), 1 << 26)
+            comm = Communicator(P, None, arena_bytes)
     else:
         if comm is None:
             import torch.distributed as dist
@@ -311,18 +317,20 @@ def setup_distributed(a, ranks=None, bounds=None, n=None, comm=None, config=Aggr
         if not comm.virtual and not _fail_together(comm, ok):
             if ok:
                 _lib.load().uaamg_dhier_free(h)
-            comm.close(collective=False)
+            if owns:
+                comm.close(collective=False)
             if ok:
                 raise RuntimeError("sharded setup failed on another rank")
     if not ok:
-        comm.close(collective=False)
+        if owns:
+            comm.close(collective=False)
         _lib.check_code(*err)
-    dh = DistributedHierarchy(comm, h)
+    dh = DistributedHierarchy(comm, h, owns_comm=owns)
     dh.row_bounds = bounds
     return dh
 
 
-def npcg_solve_distributed(dh, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None):
+def npcg_solve_distributed(dh, cycle_spec, smoother, b, tol=1e-6, max_iters=200, x0=None, use_graphs=True):
     """Collective NPCG solve (U/solvers.py:190-255) on a DistributedHierarchy.
 
     Virtual ranks: ``b`` / ``x0`` / the returned x are whole vectors.  One
@@ -349,7 +357,7 @@ def npcg_solve_distributed(dh, cycle_spec, smoother, b, tol=1e-6, max_iters=200,
     m = len(pieces)
     VP = ctypes.c_void_p * m
     hist = np.zeros(int(max_iters) + 1)
-    P = _params(cycle_spec, smoother, tol, max_iters, False)
+    P = _params(cycle_spec, smoother, tol, max_iters, use_graphs)
     res = _lib.SolveResult()
     rc = _lib.load().uaamg_dsolve(dh._h, ctypes.byref(P), VP(*[ptr(t) for t in bs]),
                                   VP(*[ptr(t) for t in x0s]) if x0s is not None else None,

@@ -111,3 +111,34 @@ def test_c3_literal_graph_stagnates_like_the_reference(U):
     with pytest.raises(U.SetupError) as ei:
         U.setup(A)
     assert str(ei.value) == str(g["setup_error"])
+
+
+def test_c5_sharded_over_8_ranks(U):
+    """The north star's target problem, C5 (512^3), row-partitioned over 8
+    ranks (virtual ranks on this one GPU -- the same sharded setup and solve
+    code as one process per GPU): every level's hierarchy SHA-identical to
+    the oracle's, the oracle's 64 iterations, history within 1e-10."""
+    name = "oracle_c5_grid3d7_512"
+    if not _have(name):
+        pytest.skip(f"{name}.npz not generated")
+    from paper_1302_2547_b200 import distributed as D
+    from paper_1302_2547_b200 import problems
+    g = load(name)
+    A = problems.grid3d_device(512, 7)
+    dh = D.setup_distributed(A, ranks=8)
+    assert dh.n_levels == int(g["n_levels"]) and dh.n_sharded >= 2
+    for l in range(dh.n_levels):
+        n, nnz = dh.level_size(l)
+        assert n == int(g[f"L{l}_n"]) and nnz == int(g[f"L{l}_nnz"]), f"level {l} size"
+        if l > 0:
+            m = dh.level_matrix(l)
+            assert sha(m.indptr, m.indices, m.data) == str(g[f"L{l}_csr_sha"]), f"level {l} matrix differs"
+        agg = dh.level_aggregation(l)
+        if agg is not None:
+            assert sha(agg[0]) == str(g[f"L{l}_v2a_sha"]) and sha(agg[1]) == str(g[f"L{l}_seeds_sha"]), f"level {l}"
+    del A
+    b = torch.ones(dh.n, dtype=torch.float64, device="cuda")
+    x, rep = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500)
+    assert_history_close(rep.residual_history, g, rtol=1e-10)
+    assert rep.iterations == int(g["iterations"])
+    dh.close()

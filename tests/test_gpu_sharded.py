@@ -109,26 +109,30 @@ def test_sharded_x0_and_jacobi(U, D):
 
 
 def test_sharded_repeat_is_bit_reproducible(U, D):
+    """Repeated solves, and graph replays vs plain launches, give the same bits."""
     ip, ix, a, g = problem_for("rgg_20000")
     dh = D.setup_distributed(_smat(U, ip, ix, a), ranks=3, shard_rows=500)
     b = np.ones(ip.shape[0] - 1)
-    r = [D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=1e-8)[1].residual_history
-         for _ in range(3)]
-    assert r[0] == r[1] == r[2]
+    r = [D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=1e-8, use_graphs=k != 1)
+         for k in range(3)]
+    assert r[0][1].residual_history == r[1][1].residual_history == r[2][1].residual_history
+    assert np.array_equal(r[0][0], r[1][0]) and np.array_equal(r[0][0], r[2][0])
 
 
 def test_sharded_c2_full_size(U, D):
-    """C2 (128^3) over 8 ranks with the default shard_rows: levels 0 and 1
-    sharded, the rest replicated; hierarchy SHA-identical to the
-    reference's, history within 1e-10."""
+    """C2 (128^3) over 8 ranks: level 0 sharded (default shard_rows = 2^20),
+    or levels 0 and 1 (shard_rows = 2^18), the rest replicated; hierarchy
+    SHA-identical to the reference's, history within 1e-10."""
     ip, ix, a, g = problem_for("c2_grid3d7_128")
-    dh = D.setup_distributed(_smat(U, ip, ix, a), ranks=8)
-    assert dh.n_sharded == 2
-    assert_hierarchy_equal(g, _levels(dh))
-    xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=1e-8,
-                                      max_iters=500)
-    assert_history_close(rs.residual_history, g, rtol=1e-10)
-    assert rs.iterations == int(g["iterations"])
+    for shard_rows, ns in ((1 << 20, 1), (1 << 18, 2)):
+        dh = D.setup_distributed(_smat(U, ip, ix, a), ranks=8, shard_rows=shard_rows)
+        assert dh.n_sharded == ns
+        assert_hierarchy_equal(g, _levels(dh))
+        xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=1e-8,
+                                          max_iters=500)
+        assert_history_close(rs.residual_history, g, rtol=1e-10)
+        assert rs.iterations == int(g["iterations"])
+        dh.close()
 
 
 def test_sharded_errors(U, D):
