@@ -315,6 +315,16 @@ int uaamg_csr_view(const uaamg_csr *c, int *n_rows, int *n_cols, int64_t *nnz, i
                    double **val);
 void uaamg_csr_free(uaamg_csr *c);
 
+/* Host <-> device transfers of the reference-layout host arrays (pageable
+ * numpy memory): pipelined through a pinned staging ring filled by host
+ * threads.  uaamg_h2d copies count elements of src_elem bytes into dst as
+ * dst_elem bytes -- equal sizes copy, 8 -> 4 narrows int64 -> int32 (the
+ * reference's indices to the device layout).  uaamg_d2h copies bytes.  Both
+ * are ordered on `stream` and return when the host buffer may be reused /
+ * read. */
+int uaamg_h2d(void *dst, const void *src, int64_t count, int src_elem, int dst_elem, void *stream);
+int uaamg_d2h(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Level-0 row partition of the sharded setup (host-only helper): P equal
  * 128-row-aligned blocks. */
 int uaamg_partition_rows(int n, int nranks, int *bounds);

@@ -106,6 +106,8 @@ _SIGS = {
     "uaamg_dhier_level": (_i, [_vp, _i, _i, ctypes.POINTER(DLevelView)]),
     "uaamg_dsolve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
     "uaamg_partition_rows": (_i, [_i, _i, _vp]),
+    "uaamg_h2d": (_i, [_vp, _vp, _i64, _i, _i, _vp]),
+    "uaamg_d2h": (_i, [_vp, _vp, _i64, _vp]),
     "uaamg_coarse_bounds": (_i, [_vp, _i, _vp]),
     "uaamg_gen_grid3d": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "uaamg_gen_grid3d_rows": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),

@@ -1,7 +1,8 @@
 // csr_tma.cuh -- TMA-pipelined CSR row kernel for the large (HBM-bound)
 // levels.
 //
-// Persistent CTAs of kTmaRows threads walk 128-row tiles.  Thread 0 streams
+// Persistent CTAs of kTmaThreads threads walk R-row tiles (128; 64 for
+// dense rows such as the 27-point stencil's).  Thread 0 streams
 // each tile's row_ptr / col / val slices into a kTmaStages-deep shared-memory
 // ring with cp.async.bulk (completion on an mbarrier), kTmaStages-1 tiles
 // ahead of the tile being computed, so the matrix stream (12 B per nonzero,
@@ -18,7 +19,8 @@
 
 namespace uaamg {
 
-constexpr int kTmaRows = 128;      // rows per tile = threads per CTA
+constexpr int kTmaThreads = 128;   // threads per CTA
+constexpr int kTmaRows = 128;      // rows per tile (default); 64 for dense rows (27-point)
 constexpr int kTmaStages = 3;
 constexpr int kTmaMaxCap = 2048;   // max nonzeros per tile on this path
 constexpr int kTmaBatch = 8;       // gathers in flight per thread
@@ -26,15 +28,17 @@ constexpr int kTmaBatch = 8;       // gathers in flight per thread
 struct TmaLayout {
     int rp_off, ci_off, av_off, stage;
 };
-__host__ __device__ inline TmaLayout tma_layout(int cap) {
+__host__ __device__ inline TmaLayout tma_layout(int cap, int rows = kTmaRows) {
     TmaLayout L;
     L.rp_off = 0;
-    L.ci_off = ((kTmaRows + 8) * 4 + 127) & ~127;
+    L.ci_off = ((rows + 8) * 4 + 127) & ~127;
     L.av_off = L.ci_off + (((cap + 8) * 4 + 127) & ~127);
     L.stage = L.av_off + (((cap + 4) * 8 + 127) & ~127);
     return L;
 }
-inline size_t tma_smem_bytes(int cap) { return (size_t)kTmaStages * tma_layout(cap).stage + 16 * kTmaStages; }
+inline size_t tma_smem_bytes(int cap, int rows = kTmaRows) {
+    return (size_t)kTmaStages * tma_layout(cap, rows).stage + 16 * kTmaStages;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
@@ -60,12 +64,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
 
-template <class Src, class Epi, bool Unit>
-__global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, int ntiles, int cap, Src src_p, Epi epi_p) {
+// R rows per tile (<= kTmaThreads): the gathers of a tile are spread over
+// all kTmaThreads threads, row folds are done by threads [0, R).
+template <class Src, class Epi, bool Unit, int R = kTmaRows>
+__global__ void __launch_bounds__(kTmaThreads) k_csr_tma(Csr A, int base, int end, int ntiles, int cap, Src src_p,
+                                                         Epi epi_p) {
+    static_assert(R <= kTmaThreads && R % 4 == 0, "tile rows");
     extern __shared__ __align__(128) unsigned char smem[];
     Epi epi = epi_p;
     Src src = src_p;
-    const TmaLayout Ly = tma_layout(cap);
+    const TmaLayout Ly = tma_layout(cap, R);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kTmaStages * Ly.stage);
     const int t = threadIdx.x;
     const int G = gridDim.x;
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
         const int tile = blockIdx.x + j * G;
         const int s = j % kTmaStages;
         unsigned char* st = smem + s * Ly.stage;
-        const int r0 = base + tile * kTmaRows, r1 = min(r0 + kTmaRows, end);
+        const int r0 = base + tile * R, r1 = min(r0 + R, end);
         const int ra = r0 & ~3;  // 16-byte aligned row_ptr slice start
         const unsigned brp = round16((unsigned)(r1 - ra + 1) * 4u);
         const int ea = e0 & ~3, eb = e0 & ~1;
@@ -94,9 +102,9 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
         if (bav) bulk_g2s(st + Ly.av_off, A.av + eb, bav, &mbar[s]);
     };
     auto bounds = [&](int j, int& e0, int& e1) {
-        const int r0 = base + (blockIdx.x + j * G) * kTmaRows;
+        const int r0 = base + (blockIdx.x + j * G) * R;
         e0 = __ldg(A.rp + r0);
-        e1 = __ldg(A.rp + min(r0 + kTmaRows, end));
+        e1 = __ldg(A.rp + min(r0 + R, end));
     };
     int ne0 = 0, ne1 = 0;  // producer: bounds of the next tile to issue
     // the matrix is read-only: its first tiles stream in before the
@@ -119,9 +127,9 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
     }
     src.init();
     // per-row operands may have been written by the predecessor: after the wait
-    if (my > 0 && base + blockIdx.x * kTmaRows + t < end) {
-        epi.pre(base + blockIdx.x * kTmaRows + t);
-        src.pre(base + blockIdx.x * kTmaRows + t);
+    if (my > 0 && t < R && base + blockIdx.x * R + t < end) {
+        epi.pre(base + blockIdx.x * R + t);
+        src.pre(base + blockIdx.x * R + t);
     }
     // Software pipeline over this CTA's tiles: iteration j folds tile j
     // (products already in its stage) while the gathers of tile j + 1 are
@@ -132,16 +140,16 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
     auto gather_issue = [&](int jj) {
         const int s = jj % kTmaStages;
         const unsigned char* st = smem + s * Ly.stage;
-        const int r0 = base + (blockIdx.x + jj * G) * kTmaRows;
+        const int r0 = base + (blockIdx.x + jj * G) * R;
         const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off) + (r0 & 3);
         const int* cis = reinterpret_cast<const int*>(st + Ly.ci_off);
         mbar_wait(&mbar[s], (unsigned)((jj / kTmaStages) & 1));
         gb = rps[0];
-        ge = rps[min(kTmaRows, end - r0)];
+        ge = rps[min(R, end - r0)];
         gea = gb & ~3;
 #pragma unroll
         for (int q = 0; q < kTmaBatch; ++q) {
-            const int e = gb + t + q * kTmaRows;
+            const int e = gb + t + q * kTmaThreads;
             v[q] = e < ge ? src(cis[e - gea]) : 0.0;
         }
     };
@@ -153,17 +161,17 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
         const int* cis = reinterpret_cast<const int*>(st + Ly.ci_off);
         double* avs = reinterpret_cast<double*>(st + Ly.av_off);
         const int eb = gb & ~1;
-        for (int base = gb + t;; base += kTmaRows * kTmaBatch) {
+        for (int base = gb + t;; base += kTmaThreads * kTmaBatch) {
 #pragma unroll
             for (int q = 0; q < kTmaBatch; ++q) {
-                const int e = base + q * kTmaRows;
+                const int e = base + q * kTmaThreads;
                 if (e < ge) avs[e - eb] = Unit ? v[q] : __dmul_rn(avs[e - eb], v[q]);
             }
-            const int nb = base + kTmaRows * kTmaBatch;
+            const int nb = base + kTmaThreads * kTmaBatch;
             if (nb >= ge) break;
 #pragma unroll
             for (int q = 0; q < kTmaBatch; ++q) {
-                const int e = nb + q * kTmaRows;
+                const int e = nb + q * kTmaThreads;
                 v[q] = e < ge ? src(cis[e - gea]) : 0.0;
             }
         }
@@ -181,16 +189,16 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
         }
         const int s = j % kTmaStages;
         const unsigned char* st = smem + s * Ly.stage;
-        const int r0 = base + (blockIdx.x + j * G) * kTmaRows;
+        const int r0 = base + (blockIdx.x + j * G) * R;
         const int* rps = reinterpret_cast<const int*>(st + Ly.rp_off) + (r0 & 3);
         const double* avs = reinterpret_cast<const double*>(st + Ly.av_off);
-        const int rows = min(kTmaRows, end - r0);
+        const int rows = min(R, end - r0);
         const int i = r0 + t;
         const bool valid = t < rows;
         if (j + 1 < my) {
             // next tile's row operands and first gather batch go out now
-            const int i1 = r0 + G * kTmaRows + t;
-            if (i1 < end) {
+            const int i1 = r0 + G * R + t;
+            if (t < R && i1 < end) {
                 epi.pre(i1);
                 src.pre(i1);
             }
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kTmaRows) k_csr_tma(Csr A, int base, int end, 
     if constexpr (Epi::K > 0) {
         double v[Epi::K];
         epi.vals(v);
-        grid_reduce_finish<Epi::K, kTmaRows>(v, epi.red.partials, epi.red.ticket, [&](const double (&tt)[Epi::K]) {
+        grid_reduce_finish<Epi::K, kTmaThreads>(v, epi.red.partials, epi.red.ticket, [&](const double (&tt)[Epi::K]) {
             if (!xpublish(epi.red, tt)) epi.fin(tt);
         });
     }

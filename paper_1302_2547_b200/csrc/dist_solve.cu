@@ -183,10 +183,7 @@ void DistSolve::build() {
                 take(V_XF); take(V_RF); take(V_Z); take(V_P0); take(V_P1); take(V_AP0); take(V_AP1);
             }
             build_groups(Rr.n, Rr.rps, kSolveLongMin, W.gA[l], s, Rr.a);
-            if (Rr.n >= kTmaMinRows / 8 && W.gA[l].g.np == 0) {
-                const int cap = max_tile_nnz(Rr.n, Rr.rps, s, Rr.a);
-                if (cap <= kTmaMaxCap) W.gA[l].g.tma_cap = std::max(cap, 4);
-            }
+            if (Rr.n >= kTmaMinRows / 8 && W.gA[l].g.np == 0) set_tma(W.gA[l].g, Rr.n, Rr.rps, s, Rr.a);
             // restriction rows: own aggregates, or all of them into the
             // replicated level
             const int ca = Rr.mbase, cn = Rr.mcount;

@@ -20,7 +20,8 @@ struct Groups {
     double* part = nullptr;      // np partial sums
     int nlong = 0;               // long rows (pieces grouped by row)
     double* lval = nullptr;      // per long row: its epilogue's reduced values (kMaxLongK each)
-    int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per 128-row tile
+    int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per tile
+    int tma_rows = 128;          // rows per TMA tile (128, or 64 for dense rows)
     __host__ __device__ int units() const { return ng + np; }
 };
 // exact groups (no pieces): every row folded sequentially in reference order
@@ -49,7 +50,10 @@ constexpr int kMaxLongK = 2;
 // levels with at least this many rows take the TMA-pipelined tile kernel
 constexpr int kTmaMinRows = 65536;
 // max nonzeros over 128-row tiles (for the TMA path)
-int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0);
+int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0, int rows = 128);
+// TMA eligibility of rows [base, base + n): sets g.tma_cap / g.tma_rows
+// (128-row tiles, else 64-row tiles) when a tile's nonzeros fit the stage
+void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base = 0);
 
 // fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
 struct BetaReq {

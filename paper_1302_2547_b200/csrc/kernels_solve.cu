@@ -195,25 +195,41 @@ __global__ void k_row_bounds(int m, const int* rows, const int* rp, int2* out) {
 }
 }  // namespace
 
-__global__ void k_tile_nnz_max(int n, const int* rp, int* out) {  // rp: first row of the range
-    const int nt = (n + kTmaRows - 1) / kTmaRows;
+__global__ void k_tile_nnz_max(int n, int rows, const int* rp, int* out) {  // rp: first row of the range
+    const int nt = (n + rows - 1) / rows;
     int m = 0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
-        m = max(m, rp[min((t + 1) * kTmaRows, n)] - rp[t * kTmaRows]);
+        m = max(m, rp[min((t + 1) * rows, n)] - rp[t * rows]);
     m = block_max(m);
     if (threadIdx.x == 0) atomicMax(out, m);
 }
 
-int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base) {
+int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base, int rows) {
     rp += base;
     if (n == 0) return 0;
     DBuf<int> m(1, s);
     UA_CK(cudaMemsetAsync(m.p, 0, sizeof(int), s));
-    UA_LAUNCH(k_tile_nnz_max, std::min(cdiv(cdiv(n, kTmaRows), 256), 4 * kNumSMs), 256, 0, s, n, rp, m.p);
+    UA_LAUNCH(k_tile_nnz_max, std::min(cdiv(cdiv(n, rows), 256), 4 * kNumSMs), 256, 0, s, n, rows, rp, m.p);
     int h = 0;
     UA_CK(cudaMemcpyAsync(&h, m.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     UA_CK(cudaStreamSynchronize(s));
     return h;
+}
+
+void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base) {
+    static const bool no64 = getenv("UAAMG_NO_TMA64") != nullptr;  // A/B diagnostics
+    int cap = max_tile_nnz(n, rp, s, base, kTmaRows);
+    if (cap <= kTmaMaxCap) {
+        g.tma_cap = std::max(cap, 4);
+        g.tma_rows = kTmaRows;
+        return;
+    }
+    if (no64) return;
+    cap = max_tile_nnz(n, rp, s, base, 64);
+    if (cap <= kTmaMaxCap) {
+        g.tma_cap = std::max(cap, 4);
+        g.tma_rows = 64;
+    }
 }
 
 void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s, int base) {

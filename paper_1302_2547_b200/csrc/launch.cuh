@@ -44,6 +44,38 @@ void run_map(int n, const Body& body, Exec ex) {
 template <class Body>
 void run_map(int n, const Body& body, Exec ex);
 
+// TMA-pipelined persistent tiles of R rows (occupancy cached per device)
+template <class Src, class Epi, bool Unit, int R>
+inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
+    static int occ_dev[kMaxDevices], smem_set_dev[kMaxDevices];
+    static size_t occ_smem_dev[kMaxDevices];
+    static bool init_dev[kMaxDevices];
+    const int dev = cur_dev();
+    if (!init_dev[dev]) {
+        occ_dev[dev] = -1;
+        smem_set_dev[dev] = 0;
+        occ_smem_dev[dev] = 0;
+        init_dev[dev] = true;
+    }
+    int& occ = occ_dev[dev];
+    int& smem_set = smem_set_dev[dev];
+    size_t& occ_smem = occ_smem_dev[dev];
+    const size_t smem = tma_smem_bytes(G.tma_cap, R);
+    auto kfn = k_csr_tma<Src, Epi, Unit, R>;
+    if ((int)smem > smem_set) {
+        UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = (int)smem;
+        occ = -1;
+    }
+    if (occ < 0 || occ_smem != smem) {
+        UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaThreads, smem));
+        occ_smem = smem;
+    }
+    const int ntiles = cdiv(G.n, R);
+    const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
+    UA_LAUNCH_PDL(kfn, grid, kTmaThreads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi);
+}
+
 template <class Src, class Epi, bool Unit>
 inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
     // an empty range still launches when it must publish a (zero) reduction
@@ -52,34 +84,10 @@ inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi&
         else if (epi.red.xslot == nullptr) return;
     }
     if (G.tma_cap > 0 && G.np == 0) {
-        // large level: TMA-pipelined persistent tiles
-        static int occ_dev[kMaxDevices], smem_set_dev[kMaxDevices];
-        static size_t occ_smem_dev[kMaxDevices];
-        static bool init_dev[kMaxDevices];
-        const int dev = cur_dev();
-        if (!init_dev[dev]) {
-            occ_dev[dev] = -1;
-            smem_set_dev[dev] = 0;
-            occ_smem_dev[dev] = 0;
-            init_dev[dev] = true;
-        }
-        int& occ = occ_dev[dev];
-        int& smem_set = smem_set_dev[dev];
-        size_t& occ_smem = occ_smem_dev[dev];
-        const size_t smem = tma_smem_bytes(G.tma_cap);
-        auto kfn = k_csr_tma<Src, Epi, Unit>;
-        if ((int)smem > smem_set) {
-            UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            smem_set = (int)smem;
-            occ = -1;
-        }
-        if (occ < 0 || occ_smem != smem) {
-            UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem));
-            occ_smem = smem;
-        }
-        const int ntiles = cdiv(G.n, kTmaRows);
-        const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
-        UA_LAUNCH_PDL(kfn, grid, kTmaRows, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi);
+        // large level: TMA-pipelined persistent tiles (64-row tiles when
+        // 128 rows exceed the stage: dense stencils)
+        if (G.tma_rows == 64) launch_tma<Src, Epi, Unit, 64>(A, G, src, epi, ex);
+        else launch_tma<Src, Epi, Unit, kTmaRows>(A, G, src, epi, ex);
         return;
     }
     const int grid = std::min(cdiv(G.units(), kGrpWarps), kNumSMs * kGrpCtasPerSM);

@@ -124,10 +124,7 @@ static void finish_level(Level& L, cudaStream_t s) {
     build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s);
     static const bool no_tma = getenv("UAAMG_NO_TMA") != nullptr;  // A/B diagnostics
     static const long long tma_min = getenv("UAAMG_TMA_MIN_ROWS") ? atoll(getenv("UAAMG_TMA_MIN_ROWS")) : kTmaMinRows;
-    if (!no_tma && L.n >= tma_min && L.grp.g.np == 0) {
-        const int cap = max_tile_nnz(L.n, L.rp.p, s);
-        if (cap <= kTmaMaxCap) L.grp.g.tma_cap = std::max(cap, 4);
-    }
+    if (!no_tma && L.n >= tma_min && L.grp.g.np == 0) set_tma(L.grp.g, L.n, L.rp.p, s);
 }
 
 // aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)

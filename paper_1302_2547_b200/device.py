@@ -18,6 +18,7 @@ _TYPESTR = {np.dtype(np.int32): "<i4", np.dtype(np.float64): "<f8", np.dtype(np.
             np.dtype(np.int64): "<i8"}
 _TORCH = {np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
           np.dtype(np.int64): torch.int64}
+_NP = {v: k for k, v in _TORCH.items()}
 
 
 def cuda_device():
@@ -35,12 +36,33 @@ def ctypes_stream(s):
     return s.cuda_stream
 
 
+# host arrays at least this large go through the library's staged copies
+STAGED_MIN_BYTES = 1 << 20
+
+
+def _staged_ok(arr, dtype):
+    dt = np.dtype(dtype)
+    return (isinstance(arr, np.ndarray) and arr.flags.c_contiguous and arr.nbytes >= STAGED_MIN_BYTES
+            and (arr.dtype == dt or (arr.dtype.kind == dt.kind == "i" and arr.itemsize == 8 and dt.itemsize == 4)))
+
+
+def _staged_h2d(out, arr):
+    _lib.check(_lib.load().uaamg_h2d(out.data_ptr(), arr.ctypes.data, int(arr.shape[0]), int(arr.itemsize),
+                                     int(out.element_size()), stream()))
+    return out
+
+
 def to_device(a, dtype):
-    """numpy / torch -> contiguous device tensor of ``dtype`` (numpy dtype)."""
+    """numpy / torch -> contiguous device tensor of ``dtype`` (numpy dtype).
+    Large host arrays (e.g. the reference's int64 indices) are copied and
+    narrowed through the library's pinned staging pipeline (uaamg_h2d)."""
     dt = _TORCH[np.dtype(dtype)]
     if isinstance(a, torch.Tensor):
         return a.to(device=cuda_device(), dtype=dt).contiguous()
-    arr = np.ascontiguousarray(a, dtype=dtype)
+    arr = np.asarray(a)
+    if arr.ndim == 1 and _staged_ok(arr, dtype):
+        return _staged_h2d(torch.empty(arr.shape[0], dtype=dt, device=cuda_device()), arr)
+    arr = np.ascontiguousarray(arr, dtype=dtype)
     return _host_view(arr).to(device=cuda_device(), non_blocking=False)
 
 
@@ -74,6 +96,8 @@ def to_device_padded(a, dtype):
         return src
     if src is None:
         arr = np.asarray(a)
+        if arr.ndim == 1 and _staged_ok(arr, dtype):
+            return _staged_h2d(device_empty(arr.shape[0], dtype), arr)
         if arr.dtype != np.dtype(dtype) and arr.dtype.kind == np.dtype(dtype).kind and arr.flags.c_contiguous:
             # e.g. the reference's int64 indices -> int32: copy as is, narrow
             # on the device (cheaper than a host conversion pass)
@@ -107,7 +131,14 @@ def ptr(t):
 
 
 def to_host(t):
-    return t.detach().cpu().numpy()
+    """device tensor -> numpy (large contiguous tensors through uaamg_d2h)."""
+    t = t.detach()
+    if t.is_cuda and t.dtype in _NP and t.is_contiguous() and t.numel() * t.element_size() >= STAGED_MIN_BYTES:
+        out = np.empty(t.shape, dtype=_NP[t.dtype])
+        _lib.check(_lib.load().uaamg_d2h(out.ctypes.data, t.data_ptr(), int(t.numel() * t.element_size()),
+                                         stream()))
+        return out
+    return t.cpu().numpy()
 
 
 class _CudaView:

@@ -351,3 +351,25 @@ def test_aggregate_nonsymmetric_pattern_vs_oracle(U, oracle, seed):
         v2a, seeds = oracle.aggregate(M.indptr, M.indices, M.data, **cfg)
         assert np.array_equal(agg.vertex_to_agg, v2a)
         assert np.array_equal(agg.coarse_vertex_of_agg, seeds)
+
+
+def test_27pt_tma64_level0_vs_oracle(U, oracle):
+    """27-point rows (27 x 128 > the TMA stage) take 64-row TMA tiles; the
+    hierarchy and history must still match the oracle (rows folded in
+    reference order, bit-exact sums)."""
+    from paper_1302_2547_b200 import problems
+    A = problems.grid3d(48, 27)
+    h = U.setup(A)
+    ho = oracle.setup(A.indptr, A.indices, A.data)
+    assert h.n_levels == ho.n_levels
+    for Lg, Lo in zip(h.levels[1:], ho.levels[1:]):
+        m = Lg.matrix
+        assert np.array_equal(m.indptr, Lo.indptr) and np.array_equal(m.indices, Lo.indices)
+        assert np.array_equal(m.data, Lo.data)
+    b = np.ones(A.n_rows)
+    x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-10, max_iters=300)
+    xo, ro = oracle.npcg_solve(ho, b, tol=1e-10, max_iters=300)
+    assert rep.iterations == ro.iterations
+    h1, h2 = np.array(rep.residual_history), np.array(ro.residual_history)
+    err = np.where(np.abs(h1 - h2) <= 1e-13, 0, np.abs(h1 - h2) / h2)
+    assert err.max() <= 1e-10

@@ -6,6 +6,9 @@ geometric graph (C3) on the host.  Optionally the row-partitioned solve with
 P virtual ranks is checked against the single-device history.
 
   python tools/configs_bench.py [C1 C3 C4 ...] [--sharded P]
+
+(--sharded P: the row-partitioned setup + solve with P virtual ranks,
+checked against the single-device history)
 """
 import ctypes
 import json
@@ -36,11 +39,12 @@ def build(name):
         A = problems.grid3d_device(128, 7)
         desc = "3D 7-point 128^3"
     elif name == "C3":
-        A = DeviceCSR.from_host(problems.random_geometric(1 << 23, 12.0, seed=0))
-        # with the default n0 = 100 the reference itself stops with
+        # the literal SURVEY 8d graph makes the reference itself stop with
         # SetupError at level 5 (190 isolated vertices cannot coarsen;
-        # reproduced bit-for-bit here and by the oracle), so C3 runs n0 = 256
-        desc = "random geometric graph, 8,388,608 vertices, degree ~12, setup(n0=256)"
+        # reproduced bit-for-bit here and by the oracle, tests/test_gpu_fullsize.py);
+        # the solvable C3 is its largest connected component
+        A = DeviceCSR.from_host(problems.random_geometric(1 << 23, 12.0, seed=0, largest_component=True))
+        desc = "random geometric graph, 2^23 points, degree ~12, largest connected component (8,388,396 vertices)"
     elif name == "C4":
         A = problems.grid3d_device(256, 27)
         desc = "3D 27-point 256^3 (single GPU)"
@@ -69,7 +73,7 @@ def solve(h, b, profile):
     return x, res, hist[: res.iterations + 1]
 
 
-SETUP_KW = {"C3": {"n0": 256}}
+SETUP_KW = {}
 
 
 def run(name, sharded):
@@ -110,7 +114,11 @@ def run(name, sharded):
            "steps_s": [round(s[0], 4) for s in steps], "level0_kernels": kern,
            "grid_complexity": round(h.grid_complexity, 4), "operator_complexity": round(h.operator_complexity, 4)}
     if sharded:
-        xs, rs = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500, ranks=sharded)
+        from paper_1302_2547_b200 import distributed as D
+        del h
+        dh = D.setup_distributed(A, ranks=sharded)
+        xs, rs = D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), b, tol=1e-8, max_iters=500)
+        dh.close()
         h1 = np.asarray(hist)
         hs = np.asarray(rs.residual_history)
         out["sharded"] = {"ranks": sharded, "iterations": rs.iterations,

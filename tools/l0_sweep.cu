@@ -6,6 +6,7 @@
 // bandwidth part (t = t0 + bytes / BW).
 // Build + run: tools/l0_sweep.sh [stencil]
 #include <cstdio>
+#include <type_traits>
 #include <vector>
 
 #include "../paper_1302_2547_b200/csrc/csr_group.cuh"
@@ -115,22 +116,24 @@ int main(int argc, char** argv) {
             const int grid = std::min(cdiv(G.units(), kGrpWarps), kNumSMs * kGrpCtasPerSM);
             k_csr_group<SrcVec, EpiSweep, false><<<grid, 32 * kGrpWarps>>>(A, G, SrcVec{x}, ep);
         }, bytes);
-        // max nonzeros over 128-row tiles (host: regular stencil, interior bound)
-        const int cap = st * kTmaRows;
-        if (cap <= kTmaMaxCap) {
-            const size_t smem = tma_smem_bytes(cap);
-            auto kfn = k_csr_tma<SrcVec, EpiSweep, false>;
+        // max nonzeros per tile (regular stencil: interior bound), 128- and 64-row tiles
+        auto tma = [&](auto rows_tag) {
+            constexpr int R = decltype(rows_tag)::value;
+            const int cap = st * R;
+            if (cap > kTmaMaxCap) return;
+            const size_t smem = tma_smem_bytes(cap, R);
+            auto kfn = k_csr_tma<SrcVec, EpiSweep, false, R>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaRows, smem);
-            const int ntiles = cdiv(N, kTmaRows);
-            for (int cta : {occ}) {
-                const int grid = std::min(ntiles, kNumSMs * cta);
-                char nm[64];
-                snprintf(nm, sizeof nm, "tma sweep (%d CTA/SM, %zu B)", cta, smem);
-                timeit(nm, [&] { kfn<<<grid, kTmaRows, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep); }, bytes);
-            }
-        }
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaThreads, smem);
+            const int ntiles = cdiv(N, R);
+            const int grid = std::min(ntiles, kNumSMs * occ);
+            char nm[64];
+            snprintf(nm, sizeof nm, "tma%d sweep (%d CTA/SM, %zu B)", R, occ, smem);
+            timeit(nm, [&] { kfn<<<grid, kTmaThreads, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep); }, bytes);
+        };
+        tma(std::integral_constant<int, 128>{});
+        tma(std::integral_constant<int, 64>{});
         const size_t words = (size_t)(bytes / 2) / 16;
         void *src, *dst;
         cudaMalloc(&src, words * 16 + 64);
