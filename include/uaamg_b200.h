@@ -126,6 +126,8 @@ typedef struct {
     int n0;                 /* setup(n0=100)                                     */
     int max_levels;         /* setup(max_levels=20)                              */
     int singular;           /* -1 auto (detect_singular), 0/1 forced             */
+    int reshape_sweeps;     /* setup(reshape_sweeps=0): subgraph reshaping sweeps per level */
+    int reshape_pair_cap;   /* setup(reshape_pair_cap=16): largest pair enumerated (<= 16) */
     int borrow;             /* 1: level 0 aliases the caller's arrays (they must
                                outlive the hierarchy, as the reference's Level 0
                                holds the caller's matrix, and each must have
@@ -314,6 +316,15 @@ int uaamg_assemble_laplacian(int n, int64_t m, const int64_t *ei, const int64_t 
 int uaamg_csr_view(const uaamg_csr *c, int *n_rows, int *n_cols, int64_t *nnz, int **row_ptr, int **col,
                    double **val);
 void uaamg_csr_free(uaamg_csr *c);
+
+/* U/reshaping.py:215-248 reshape_sweep on a level matrix and its
+ * aggregation (device): v2a (n) is updated in place, seeds (nc) receives the
+ * smallest member of every aggregate (U/aggregation.py:248-257); *skipped =
+ * pairs larger than pair_cap (<= 16).  UAAMG_EINVAL with the reference's
+ * message when a pair has no balanced connected split. */
+int uaamg_reshape_sweep(int n, int64_t nnz, const int *row_ptr, const int *col, const double *val, int nc, int *v2a,
+                        int *seeds, int smoother_l1, double omega, int sweeps, int pair_cap, int *skipped,
+                        void *stream);
 
 /* Host <-> device transfers of the reference-layout host arrays (pageable
  * numpy memory): pipelined through a pinned staging ring filled by host

@@ -15,6 +15,7 @@ from .graph import GraphError, GraphProblem, assemble_laplacian, assemble_laplac
 from .hierarchy import CoarseSolver, Hierarchy, Level, SetupError, detect_singular, galerkin_coarse, setup
 from .solvers import (CycleSpec, NumericalError, Smoother, SolveReport, cycle, npcg_solve, prolongate_add,
                       restrict, smooth, smoother_inverse_diag)
+from .reshaping import DisconnectedPair, PairTooLarge, reshape_sweep
 from .sparse import SparseFormatError, SparseMatrix, squared_adjacency_pattern
 
 __version__ = "0.1.0"
@@ -26,6 +27,7 @@ __all__ = [
     "CycleSpec", "NumericalError", "Smoother", "SolveReport", "cycle", "npcg_solve", "prolongate_add", "restrict",
     "smooth", "smoother_inverse_diag",
     "SparseMatrix", "SparseFormatError", "DeviceCSR", "squared_adjacency_pattern",
+    "reshape_sweep", "DisconnectedPair", "PairTooLarge",
     "TwoLevelReport", "hierarchy_report", "q_energy_norm", "reports_to_csv", "two_level_rate",
     "GraphError", "GraphProblem", "assemble_laplacian", "assemble_laplacian_device", "generate_structured_grid",
     "__version__",

@@ -29,7 +29,8 @@ _d = ctypes.c_double
 
 class SetupParams(ctypes.Structure):
     _fields_ = [("size_cap", _i64), ("seed", _u64), ("max_passes", _i), ("passes_per_level", _i),
-                ("n0", _i), ("max_levels", _i), ("singular", _i), ("borrow", _i)]
+                ("n0", _i), ("max_levels", _i), ("singular", _i), ("reshape_sweeps", _i),
+                ("reshape_pair_cap", _i), ("borrow", _i)]
 
 
 class HierarchyInfo(ctypes.Structure):
@@ -107,6 +108,7 @@ _SIGS = {
     "uaamg_dsolve": (_i, [_vp, ctypes.POINTER(SolveParams), _vp, _vp, _vp, _vp, ctypes.POINTER(SolveResult), _vp]),
     "uaamg_partition_rows": (_i, [_i, _i, _vp]),
     "uaamg_h2d": (_i, [_vp, _vp, _i64, _i, _i, _vp]),
+    "uaamg_reshape_sweep": (_i, [_i, _i64, _vp, _vp, _vp, _i, _vp, _vp, _i, _d, _i, _i, _vp, _vp]),
     "uaamg_d2h": (_i, [_vp, _vp, _i64, _vp]),
     "uaamg_coarse_bounds": (_i, [_vp, _i, _vp]),
     "uaamg_gen_grid3d": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),

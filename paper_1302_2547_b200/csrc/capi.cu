@@ -47,6 +47,18 @@ int uaamg_gen_grid3d(int nx, int ny, int nz, int stencil, int neumann, int* row_
     })
 }
 
+int uaamg_reshape_sweep(int n, int64_t nnz, const int* row_ptr, const int* col, const double* val, int nc, int* v2a,
+                        int* seeds, int smoother_l1, double omega, int sweeps, int pair_cap, int* skipped,
+                        void* stream) {
+    UA_GUARD({
+        Csr A = make_csr(n, row_ptr, col, val);
+        A.nnz = (int)nnz;
+        const int k = device_reshape_sweep(A, nc, v2a, seeds, smoother_l1, omega, sweeps, pair_cap,
+                                           (cudaStream_t)stream);
+        if (skipped) *skipped = k;
+    })
+}
+
 int uaamg_gen_grid3d_rows(int nx, int ny, int nz, int stencil, int neumann, int row_begin, int row_end,
                           int* row_ptr, int* col, double* val, int64_t* nnz, void* stream) {
     UA_GUARD({

@@ -890,6 +890,7 @@ std::unique_ptr<DistHier> dist_setup(std::shared_ptr<Comm> Cp, int n, const int*
     if (!C.connected) throw Error(UAAMG_EINVAL, "communicator is not connected");
     if (P.size_cap > 0) throw Error(UAAMG_EUNSUPPORTED, "sharded setup supports size_cap=None only");
     if (P.passes_per_level != 1) throw Error(UAAMG_EUNSUPPORTED, "sharded setup supports passes_per_level=1 only");
+    if (P.reshape_sweeps > 0) throw Error(UAAMG_EUNSUPPORTED, "sharded setup supports reshape_sweeps=0 only");
     if (P.max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
     cudaStream_t s = C.s;

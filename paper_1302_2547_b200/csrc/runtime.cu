@@ -152,6 +152,10 @@ static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t 
         nc = nc2;
         seeds = std::move(s2);
     }
+    if (P.reshape_sweeps > 0) {
+        // U/hierarchy.py:141-144: reshape the level's aggregation (l1 local smoother)
+        device_reshape_sweep(L.csr(), nc, L.v2a.p, seeds.p, 1, 2.0 / 3.0, P.reshape_sweeps, P.reshape_pair_cap, s);
+    }
     L.nc = nc;
     L.seeds.alloc(std::max(nc, 1), s);
     UA_CK(cudaMemcpyAsync(L.seeds.p, seeds.p, sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));

@@ -15,6 +15,10 @@ void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cu
 long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
                           DBuf<int>& rp_c, DBuf<int>& ci_c, DBuf<double>& av_c, cudaStream_t s);
 int device_coarse_factor(const Csr& A, bool singular, DBuf<double>& Minv, cudaStream_t s);
+// subgraph reshaping sweeps (reshape.cu): v2a updated in place, seeds =
+// smallest members; returns the number of pairs skipped (> pair_cap)
+int device_reshape_sweep(const Csr& A, int nc, int* v2a, int* seeds, int l1, double omega, int sweeps, int pair_cap,
+                         cudaStream_t s);
 
 // kernel-table helpers
 void launch_select_pattern(const Csr& P, const double* s_, const uint8_t* processed, uint8_t* out, cudaStream_t s);

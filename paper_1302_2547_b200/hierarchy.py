@@ -229,9 +229,8 @@ def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0
     ``a``: host SparseMatrix (uploaded once) or DeviceCSR (used in place)."""
     if a.n_rows != a.n_cols:
         raise SetupError("matrix must be square")
-    if reshape_sweeps > 0:
-        raise NotImplementedError("subgraph reshaping (reshape_sweeps > 0) is outside the B200 hot path "
-                                  "(SURVEY.md section 8f, rank 4)")
+    if reshape_sweeps > 0 and reshape_pair_cap > 16:
+        raise NotImplementedError("reshape_pair_cap > 16: the device enumeration handles pairs of at most 16 vertices")
     d = a if isinstance(a, DeviceCSR) else a.device()
     # level 0 aliases the caller's device arrays when the TMA tile kernel may
     # read them in place (int32/int32/float64, contiguous, 16-byte aligned,
@@ -244,9 +243,14 @@ def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0
     P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
                          max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
                          n0=int(n0), max_levels=int(max_levels),
-                         singular=-1 if singular is None else int(bool(singular)), borrow=int(borrow))
+                         singular=-1 if singular is None else int(bool(singular)),
+                         reshape_sweeps=int(reshape_sweeps), reshape_pair_cap=int(reshape_pair_cap), borrow=int(borrow))
     h = ctypes.c_void_p()
-    _lib.check(_lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
-                                       ctypes.byref(h), stream()))
+    rc = _lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
+                                 ctypes.byref(h), stream())
+    if rc == _lib.UAAMG_EINVAL and reshape_sweeps > 0:
+        from .reshaping import _raise_reshape_error
+        _raise_reshape_error(_lib.last_error())
+    _lib.check(rc)
     # level 0 aliases the device matrix (as the reference's Level 0 holds A)
     return Hierarchy(h, matrix_owner=d)

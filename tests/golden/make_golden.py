@@ -261,6 +261,41 @@ def make_hierarchy(U, name, A, cfg_kw=None, setup_kw=None, solves=(), full=True,
     return h
 
 
+def make_reshape(U, P):
+    """Subgraph reshaping (reference reshaping.py:215-248): aggregations
+    before / after 1 and 2 sweeps, and a setup(reshape_sweeps=1) hierarchy
+    with its solve history."""
+    print("reshape")
+    out = {}
+    cases = {
+        "g2d16_t5": (P.grid2d(16), U.AggregationConfig(size_cap=5)),       # DisconnectedPair in the reference
+        "g2d16_t4": (P.grid2d(16), U.AggregationConfig(size_cap=4)),
+        "g2d12": (P.grid2d(12), U.AggregationConfig()),
+        "g3d6_t6": (P.grid3d(6, 7), U.AggregationConfig(size_cap=6, seed=1)),
+        "g3d6_27_t6": (P.grid3d(6, 27), U.AggregationConfig(size_cap=6)),
+        "wgraph_t6": (random_weighted_problem(U, 3000, 4), U.AggregationConfig(size_cap=6, seed=2)),
+    }
+    for tag, (A, cfg) in cases.items():
+        if not isinstance(A, U.SparseMatrix):
+            A = U.SparseMatrix(A.n_rows, A.n_cols, A.indptr, A.indices, A.data)
+        agg = U.aggregate(A, cfg)
+        out[tag + "_indptr"], out[tag + "_indices"], out[tag + "_data"] = A.indptr, A.indices, A.data
+        out[tag + "_v2a"], out[tag + "_seeds"] = agg.vertex_to_agg, agg.coarse_vertex_of_agg
+        for key, kw in (("rs1", dict(sweeps=1)), ("rs2", dict(sweeps=2)),
+                        ("rsj", dict(sweeps=1, smoother=U.Smoother("jacobi"))), ("rs1c8", dict(sweeps=1, pair_cap=8))):
+            try:
+                r = U.reshape_sweep(A, agg, **kw)
+                out[f"{tag}_{key}_v2a"], out[f"{tag}_{key}_seeds"] = r.vertex_to_agg, r.coarse_vertex_of_agg
+                res = "ok"
+            except ValueError as e:  # DisconnectedPair (the reference raises it from reshape_sweep)
+                out[f"{tag}_{key}_error"] = np.array(f"{type(e).__name__}: {e}")
+                res = f"{type(e).__name__}"
+            print(f"  {tag} {key}: n={A.n_rows} nc={agg.n_coarse} {res}")
+    save("reshape", **out)
+    make_hierarchy(U, "g2d_dir_20_t4_rs1", P.grid2d(20), cfg_kw={"size_cap": 4, "seed": 1},
+                   setup_kw={"reshape_sweeps": 1, "n0": 50}, solves=[("", {})])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c2", action="store_true")
@@ -321,6 +356,8 @@ def main():
         # (tests/golden/make_oracle_fixtures.py)
         make_hierarchy(U, "rgg_lcc_262144", P.random_geometric(1 << 18, 12.0, 0, largest_component=True),
                        solves=[("", {})], full=False)
+    if want("reshape"):
+        make_reshape(U, P)
     if want("small"):
         make_hierarchy(U, "g2d_dir_12_n0", P.grid2d(12), setup_kw={"n0": 200}, solves=[("", {})])
         make_hierarchy(U, "g2d_dir_16_ml2", P.grid2d(16), setup_kw={"max_levels": 2}, solves=[("", {})])
