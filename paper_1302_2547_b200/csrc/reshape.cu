@@ -26,6 +26,8 @@
 // (U/aggregation.py:248-257).
 #include <cub/cub.cuh>
 
+#include <math_constants.h>
+
 #include <vector>
 
 #include "setup.h"
@@ -240,11 +242,13 @@ __global__ void __launch_bounds__(kRsThreads) k_reshape_pairs(Csr A, int npairs,
     double amax = 0.0;
     for (int i = 0; i < m; ++i)
         for (int j = 0; j < m; ++j) amax = fmax(amax, fabs(ah[i][j]));
-    // |T|^2 of split rank r; < 0: not a candidate (a side is disconnected)
+    // |T|^2 of split rank r (the reference's rank_one_trace may be negative);
+    // -inf: not a candidate (a side is disconnected)
+    const double kNone = -CUDART_INF;
     auto score = [&](long long r) -> double {
         const unsigned s1 = even ? (1u | (unrank(r, m - 1, half - 1) << 1)) : unrank(r, m, half);
         const unsigned s2 = all & ~s1;
-        if (!connected(s1, adj) || !connected(s2, adj)) return -1.0;
+        if (!connected(s1, adj) || !connected(s2, adj)) return kNone;
         const int n1 = __popc(s1), n2 = m - n1;
         double w[kRsMax], y[kRsMax], u[kRsMax];
         for (int k = 0; k < m; ++k) w[k] = ((s1 >> k) & 1) ? 1.0 / n1 : -1.0 / n2;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reshape_pairs(Csr A, int npairs,
             y[i] = a;
             waw += w[i] * a;
         }
-        if (!(waw > 1e-14 * fmax(amax, 1.0))) return -1.0;  // zero-energy coarse vector (disconnected union)
+        if (!(waw > 1e-14 * fmax(amax, 1.0))) return kNone;  // zero-energy coarse vector (disconnected union)
         double umax = 0.0, uu = 0.0;
         for (int i = 0; i < m; ++i) {
             double a = 0.0;
@@ -281,23 +285,23 @@ __global__ void __launch_bounds__(kRsThreads) k_reshape_pairs(Csr A, int npairs,
         return 0.0;
     };
     // pass 1: the maximum; pass 2: the earliest split within 1e-10 of it
-    double best = -1.0;
+    double best = kNone;
     for (long long r = t; r < ncand; r += blockDim.x) best = fmax(best, score(r));
     bt[t] = best;
     __syncthreads();
     __shared__ double tmax_s;
     if (t == 0) {
-        double tm = -1.0;
+        double tm = kNone;
         for (int k = 0; k < (int)blockDim.x; ++k) tm = fmax(tm, bt[k]);
         tmax_s = tm;
     }
     __syncthreads();
     const double tmax = tmax_s;
     long long first = -1;
-    if (tmax >= 0.0)
+    if (tmax > kNone)
         for (long long r = t; r < ncand; r += blockDim.x) {
             const double v = score(r);
-            if (v >= 0.0 && v >= tmax - 1e-10 * fabs(tmax)) {
+            if (v > kNone && v >= tmax - 1e-10 * fabs(tmax)) {
                 first = r;
                 break;
             }
