@@ -24,6 +24,7 @@ constexpr int kTmaRows = 128;      // rows per tile (default); 64 for dense rows
 constexpr int kTmaStages = 3;
 constexpr int kTmaMaxCap = 2048;   // max nonzeros per tile on this path
 constexpr int kTmaBatch = 8;       // gathers in flight per thread
+constexpr double kStreamHintBytes = 64.0 * 1024 * 1024;  // matrix streams above this load L2 evict-first
 
 struct TmaLayout {
     int rp_off, ci_off, av_off, stage;
@@ -62,13 +63,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(m))
         : "memory");
 }
+// same with an L2 cache policy (evict_first: a matrix stream larger than L2
+// should not push the coarse levels and the vectors out of it)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* m, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ unsigned round16(unsigned b) { return (b + 15u) & ~15u; }
 
 // R rows per tile (<= kTmaThreads): the gathers of a tile are spread over
 // all kTmaThreads threads, row folds are done by threads [0, R).
 template <class Src, class Epi, bool Unit, int R = kTmaRows>
 __global__ void __launch_bounds__(kTmaThreads) k_csr_tma(Csr A, int base, int end, int ntiles, int cap, Src src_p,
-                                                         Epi epi_p) {
+                                                         Epi epi_p, int stream_hint) {
     static_assert(R <= kTmaThreads && R % 4 == 0, "tile rows");
     extern __shared__ __align__(128) unsigned char smem[];
     Epi epi = epi_p;
@@ -97,9 +111,16 @@ __global__ void __launch_bounds__(kTmaThreads) k_csr_tma(Csr A, int base, int en
         const unsigned bav = Unit ? 0u : round16((unsigned)(e1 - eb) * 8u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&mbar[s], brp + bci + bav);
-        bulk_g2s(st + Ly.rp_off, A.rp + ra, brp, &mbar[s]);
-        if (bci) bulk_g2s(st + Ly.ci_off, A.ci + ea, bci, &mbar[s]);
-        if (bav) bulk_g2s(st + Ly.av_off, A.av + eb, bav, &mbar[s]);
+        if (stream_hint) {
+            const uint64_t pol = policy_evict_first();
+            bulk_g2s_hint(st + Ly.rp_off, A.rp + ra, brp, &mbar[s], pol);
+            if (bci) bulk_g2s_hint(st + Ly.ci_off, A.ci + ea, bci, &mbar[s], pol);
+            if (bav) bulk_g2s_hint(st + Ly.av_off, A.av + eb, bav, &mbar[s], pol);
+        } else {
+            bulk_g2s(st + Ly.rp_off, A.rp + ra, brp, &mbar[s]);
+            if (bci) bulk_g2s(st + Ly.ci_off, A.ci + ea, bci, &mbar[s]);
+            if (bav) bulk_g2s(st + Ly.av_off, A.av + eb, bav, &mbar[s]);
+        }
     };
     auto bounds = [&](int j, int& e0, int& e1) {
         const int r0 = base + (blockIdx.x + j * G) * R;

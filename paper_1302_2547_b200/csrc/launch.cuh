@@ -73,7 +73,10 @@ inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi&
     }
     const int ntiles = cdiv(G.n, R);
     const int grid = std::max(1, std::min(ntiles, kNumSMs * std::max(occ, 1)));
-    UA_LAUNCH_PDL(kfn, grid, kTmaThreads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi);
+    // matrix streams larger than half the L2 are loaded evict-first
+    static const bool no_hint = getenv("UAAMG_NO_L2HINT") != nullptr;  // A/B diagnostics
+    const int hint = !no_hint && 12.0 * (double)G.tma_cap * ntiles > kStreamHintBytes;
+    UA_LAUNCH_PDL(kfn, grid, kTmaThreads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi, hint);
 }
 
 template <class Src, class Epi, bool Unit>

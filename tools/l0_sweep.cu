@@ -130,7 +130,7 @@ int main(int argc, char** argv) {
             const int grid = std::min(ntiles, kNumSMs * occ);
             char nm[64];
             snprintf(nm, sizeof nm, "tma%d sweep (%d CTA/SM, %zu B)", R, occ, smem);
-            timeit(nm, [&] { kfn<<<grid, kTmaThreads, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep); }, bytes);
+            timeit(nm, [&] { kfn<<<grid, kTmaThreads, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep, 0); }, bytes);
         };
         tma(std::integral_constant<int, 128>{});
         tma(std::integral_constant<int, 64>{});
