@@ -282,7 +282,8 @@ int uaamg_dhier_level(const uaamg_dhier *d, int level, int rank, uaamg_dlevel_vi
 
 /* U/solvers.py:190-255 on a row-partitioned hierarchy, collective.  b, x0
  * (NULL or one per local rank), x: per local rank, its own rows (device).
- * Singular hierarchies are UAAMG_EUNSUPPORTED. */
+ * Singular (Neumann) hierarchies: the compatibility check and mean
+ * projections (U/solvers.py:112-125) are folded across ranks. */
 int uaamg_dsolve(uaamg_dhier *d, const uaamg_solve_params *p, const double *const *b, const double *const *x0,
                  double *const *x, double *history_host, uaamg_solve_result *res, void *stream);
 

@@ -22,7 +22,7 @@ namespace uaamg {
 
 namespace {
 
-enum VRole { V_R, V_RHS, V_E, V_TA, V_TB, V_XUP, V_XF, V_RF, V_Z, V_P0, V_P1, V_AP0, V_AP1, V_INVM, kRoles };
+enum VRole { V_R, V_RHS, V_E, V_TA, V_TB, V_XUP, V_XF, V_RF, V_Z, V_P0, V_P1, V_AP0, V_AP1, V_INVM, V_BP, kRoles };
 // outer (level-0 NPCG) vectors
 enum TRole { T_R, T_Z, T_P0, T_P1, T_AP0, T_AP1, T_X, T_B, kTRoles };
 struct VRef {
@@ -45,6 +45,8 @@ struct RankWs {
     DBuf<double> partials, hist;
     DBuf<unsigned> ticket;
     DBuf<int> bad_row;
+    DBuf<double> sums;                      // singular: 4 scratch sums per level (+ 4 spare)
+    DBuf<int> err;                          // singular: incompatible right-hand side at a coarse level
     double* slots = nullptr;                // arena: kSlotK * P (peers publish into it)
     std::unique_ptr<SolveWs> rws;           // replicated levels
 };
@@ -139,6 +141,47 @@ struct DistSolve {
 
     void build();
     bool cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int beta_state);
+    // singular (Neumann) hierarchies, U/solvers.py:112-125 across ranks
+    bool sing() const { return H.singular; }
+    double* sslot(int r, int l, int k) const { return ws[r].sums.p + 4 * l + k; }
+    // cross-rank map-reduce: every rank reduces its rows, totals folded in
+    // rank order on every rank (make(r) builds the rank's functor)
+    template <class Body, class Mk>
+    void xmap(int l, Mk&& make) {
+        sync();
+        for (int r : C.mine) {
+            Body b = make(r);
+            b.red = {rs(r).partials, rs(r).ticket};
+            xred(b.red, r);
+            run_map(nrows(r, l), b, s);
+        }
+        sync();
+        for (int r : C.mine) run_xfin(make(r), ws[r].slots, P, s);
+    }
+    void project_mean(int l, VRef v, GRef g, int k) {
+        xmap<BodySum>(l, [&](int r) {
+            BodySum b{};
+            b.v = ptr(r, v); b.slot = sslot(r, l, k); b.g = gptr(r, g);
+            return b;
+        });
+        for (int r : C.mine) {
+            BodySub sb{};
+            sb.n = L(l).n; sb.in = ptr(r, v); sb.out = ptr(r, v); sb.slot = sslot(r, l, k); sb.g = gptr(r, g);
+            run_map(nrows(r, l), sb, s);
+        }
+    }
+    void check_compatible(int l, VRef b, VRef out, GRef g) {
+        xmap<BodyCompat>(l, [&](int r) {
+            BodyCompat bc{};
+            bc.b = ptr(r, b); bc.slot = sslot(r, l, 0); bc.err = ws[r].err.p; bc.n = L(l).n; bc.g = gptr(r, g);
+            return bc;
+        });
+        for (int r : C.mine) {
+            BodySub sb{};
+            sb.n = L(l).n; sb.in = ptr(r, b); sb.out = ptr(r, out); sb.slot = sslot(r, l, 0); sb.g = gptr(r, g);
+            run_map(nrows(r, l), sb, s);
+        }
+    }
     void fcg(int l, VRef b, VRef x, GRef parent, bool begun);
     void npcg_iteration(int parity);
     void run(const std::vector<const double*>& b, const std::vector<const double*>& x0,
@@ -170,6 +213,10 @@ void DistSolve::build() {
             UA_CK(cudaStreamSynchronize(s));
         }
         W.slots = C.alloc<double>(r, (size_t)kSlotK * P);
+        W.sums.alloc(4 * (size_t)Ls + 8, s);
+        UA_CK(cudaMemsetAsync(W.sums.p, 0, sizeof(double) * (4 * Ls + 8), s));
+        W.err.alloc(1, s);
+        UA_CK(cudaMemsetAsync(W.err.p, 0, sizeof(int), s));
         W.gA.resize(Ls);
         W.gP.resize(Ls);
         for (int l = 0; l < Ls; ++l) {
@@ -177,6 +224,7 @@ void DistSolve::build() {
             const size_t n = std::max(Rr.n, 1);
             auto take = [&](VRole v) { vec[v][l][r] = C.alloc<double>(r, n); };
             take(V_INVM); take(V_R); take(V_TA); take(V_TB);
+            if (sing()) take(V_BP);
             if (p.post_sweeps > 1) take(V_XUP);
             if (l > 0) { take(V_RHS); take(V_E); }
             if (l > 0 && inner) {
@@ -239,6 +287,12 @@ void DistSolve::build() {
 // the consuming flexible CG was fused into the last sweep
 bool DistSolve::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int beta_state) {
     const int xmode = p.pre_sweeps == 0 ? 0 : 2;
+    if (sing()) {
+        // U/solvers.py:141: b = _check_compatible(b) (drift check + projection)
+        check_compatible(l, b, Lv(l, V_BP), g);
+        b = Lv(l, V_BP);
+        apprev = nullptr;  // the beta dot is not fused: z is projected first (U/solvers.py:157)
+    }
     // pre-smoothing from a zero guess, materialised (x = 0 + inv_m b, then sweeps)
     VRef cur = Lv(l, V_TA);
     if (xmode == 2) {
@@ -275,7 +329,7 @@ bool DistSolve::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int b
     const int nlev = H.nlevels();
     const bool exact = (lc == nlev - 1);
     const bool direct = !p.kcycle || p.inner_krylov_steps == 0 || exact;
-    const bool begun = !direct;
+    const bool begun = !direct && !sing();  // singular: the coarse FCG begins after the projection
     sync();
     for (int r : C.mine) {
         const int ca = R(l, r).mbase;
@@ -302,17 +356,26 @@ bool DistSolve::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int b
             run_xfin(e, ws[r].slots, P, s);
         }
     }
+    if (sing()) {
+        // U/solvers.py:150: r_c = _project_mean(restrict(r))
+        if (csh) {
+            project_mean(lc, Lv(lc, V_RHS), g, 1);
+        } else {
+            for (int r : C.mine)
+                launch_project_mean(L(l).nc, ws[r].rws->lev[0].rhs.p, sslot(r, Ls, 1), gptr(r, g), rs(r), s);
+        }
+    }
     // coarse correction
     VRef ec = Lv(lc, direct ? V_E : V_XF);
     if (csh) {
         if (direct) cycle(lc, Lv(lc, V_RHS), ec, g, nullptr, 0);
-        else fcg(lc, Lv(lc, V_RHS), ec, g, true);
+        else fcg(lc, Lv(lc, V_RHS), ec, g, begun);
     } else {
         for (int r : C.mine) {
             Plan pl = plan(r);
             LevelWs& Cw = ws[r].rws->lev[0];
             if (direct) pl.cycle(0, Cw.rhs.p, Cw.e.p, gptr(r, g));
-            else pl.fcg(0, Cw.rhs.p, Cw.xf.p, gptr(r, g), true);
+            else pl.fcg(0, Cw.rhs.p, Cw.xf.p, gptr(r, g), begun);
         }
     }
     // prolongation on own rows into tB (or tA if the pre-iterate lives in tB)
@@ -383,6 +446,7 @@ bool DistSolve::cycle(int l, VRef b, VRef out, GRef g, const VRef* apprev, int b
             run_xfin(e, ws[r].slots, P, s);
         }
     }
+    if (sing()) project_mean(l, out, g, 3);  // U/solvers.py:157
     return apprev != nullptr;
 }
 
@@ -410,7 +474,15 @@ void DistSolve::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
         GRef g{2, l, k};
         VRef rin = (k == 0) ? b : Lv(l, V_RF);
         VRef pc = Lv(l, PR[k & 1]), pp = Lv(l, PR[(k + 1) & 1]), apc = Lv(l, APR[k & 1]), app = Lv(l, APR[(k + 1) & 1]);
-        cycle(l, rin, Lv(l, V_Z), g, k > 0 ? &app : nullptr, 1);
+        const bool fused = cycle(l, rin, Lv(l, V_Z), g, k > 0 ? &app : nullptr, 1);
+        if (k > 0 && !fused) {
+            xmap<BodyBeta>(l, [&](int r) {
+                BodyBeta bb{};
+                bb.z = ptr(r, Lv(l, V_Z)); bb.pp = ptr(r, pp); bb.ap = ptr(r, app); bb.beta = &fst(r, l)->beta;
+                bb.g = gptr(r, g); bb.g2 = nullptr;
+                return bb;
+            });
+        }
         // p = z + beta p_prev on own rows, then Ap (+ p.Ap, p.r)
         for (int r : C.mine) {
             BodyDirP bp{};
@@ -437,7 +509,7 @@ void DistSolve::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
         for (int r : C.mine) {
             BodyFcgUpd body{};
             body.step = k; body.x = ptr(r, x); body.p = ptr(r, pc); body.rin = ptr(r, rin);
-            body.rout = ptr(r, Lv(l, V_RF)); body.ap = ptr(r, apc); body.st = fst(r, l); body.singular = 0;
+            body.rout = ptr(r, Lv(l, V_RF)); body.ap = ptr(r, apc); body.st = fst(r, l); body.singular = sing();
             body.red = {rs(r).partials, rs(r).ticket};
             xred(body.red, r);
             run_map(nrows(r, l), body, s);
@@ -445,8 +517,16 @@ void DistSolve::fcg(int l, VRef b, VRef x, GRef parent, bool begun) {
         sync();
         for (int r : C.mine) {
             BodyFcgUpd body{};
-            body.step = k; body.st = fst(r, l); body.singular = 0;
+            body.step = k; body.st = fst(r, l); body.singular = sing();
             run_xfin(body, ws[r].slots, P, s);
+        }
+        if (sing()) {
+            // r -= mean(r), gate from the projected norm (U/solvers.py:185-186)
+            xmap<BodyFcgProj>(l, [&](int r) {
+                BodyFcgProj pj{};
+                pj.n = L(l).n; pj.step = k; pj.r = ptr(r, Lv(l, V_RF)); pj.st = fst(r, l);
+                return pj;
+            });
         }
     }
 }
@@ -456,7 +536,16 @@ void DistSolve::npcg_iteration(int parity) {
     const TRole PR[2] = {T_P0, T_P1}, APR[2] = {T_AP0, T_AP1};
     VRef pc = O(PR[parity]), pp = O(PR[parity ^ 1]), apc = O(APR[parity]), app = O(APR[parity ^ 1]);
     GRef act{1, 0, 0};
-    cycle(0, O(T_R), O(T_Z), act, &app, 0);
+    const bool fused = cycle(0, O(T_R), O(T_Z), act, &app, 0);
+    if (sing()) project_mean(0, O(T_Z), act, 2);  // U/solvers.py:224
+    if (!fused) {
+        xmap<BodyBeta>(0, [&](int r) {
+            BodyBeta bb{};
+            bb.z = ptr(r, O(T_Z)); bb.pp = ptr(r, pp); bb.ap = ptr(r, app); bb.beta = &nst(r)->beta;
+            bb.g = gptr(r, act); bb.g2 = &nst(r)->have_prev;
+            return bb;
+        });
+    }
     for (int r : C.mine) {
         BodyDirP bp{};
         bp.src.z = ptr(r, O(T_Z)); bp.src.pprev = ptr(r, pp); bp.src.beta_p = &nst(r)->beta;
@@ -485,7 +574,7 @@ void DistSolve::npcg_iteration(int parity) {
     for (int r : C.mine) {
         BodyNpcgUpd body{};
         body.x = ptr(r, O(T_X)); body.p = ptr(r, pc); body.r = ptr(r, O(T_R)); body.ap = ptr(r, apc);
-        body.st = nst(r); body.hist = ws[r].hist.p; body.singular = 0;
+        body.st = nst(r); body.hist = ws[r].hist.p; body.singular = sing();
         body.red = {rs(r).partials, rs(r).ticket};
         xred(body.red, r);
         run_map(nrows(r, 0), body, s);
@@ -493,8 +582,21 @@ void DistSolve::npcg_iteration(int parity) {
     sync();
     for (int r : C.mine) {
         BodyNpcgUpd body{};
-        body.st = nst(r); body.hist = ws[r].hist.p; body.singular = 0;
+        body.st = nst(r); body.hist = ws[r].hist.p; body.singular = sing();
         run_xfin(body, ws[r].slots, P, s);
+    }
+    if (sing()) {
+        // x and r projected, then the norm and the bookkeeping (U/solvers.py:238-240)
+        xmap<BodyNpcgProjX>(0, [&](int r) {
+            BodyNpcgProjX bx{};
+            bx.x = ptr(r, O(T_X)); bx.st = nst(r);
+            return bx;
+        });
+        xmap<BodyNpcgProj>(0, [&](int r) {
+            BodyNpcgProj pj{};
+            pj.n = L(0).n; pj.x = ptr(r, O(T_X)); pj.r = ptr(r, O(T_R)); pj.st = nst(r); pj.hist = ws[r].hist.p;
+            return pj;
+        });
     }
 }
 
@@ -527,6 +629,21 @@ void DistSolve::run(const std::vector<const double*>& b, const std::vector<const
         else UA_CK(cudaMemsetAsync(ptr(r, O(T_X)), 0, sizeof(double) * n, s));
         UA_CK(cudaMemsetAsync(ws[r].npcg.p, 0, sizeof(NpcgState), s));
         UA_CK(cudaMemsetAsync(ws[r].fcg.p, 0, sizeof(FcgState) * std::max(Ls, 1), s));
+        UA_CK(cudaMemsetAsync(ws[r].err.p, 0, sizeof(int), s));
+        if (ws[r].rws) UA_CK(cudaMemsetAsync(ws[r].rws->err.p, 0, sizeof(int), s));
+    }
+    if (sing()) {
+        // U/solvers.py:203-204, 211-215: b projected (error if incompatible), x0 projected
+        check_compatible(0, O(T_B), O(T_B), GRef{});
+        int herr = 0;
+        for (int r : C.mine) {
+            int h = 0;
+            UA_CK(cudaMemcpyAsync(&h, ws[r].err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            UA_CK(cudaStreamSynchronize(s));
+            herr |= h;
+        }
+        if (herr) throw Error(UAAMG_ENUMERICAL, "right-hand side at the finest level has a null-space component");
+        if (have_x0) project_mean(0, O(T_X), GRef{}, 2);
     }
     sync();
     for (int r : C.mine) {
@@ -605,6 +722,21 @@ void DistSolve::run(const std::vector<const double*>& b, const std::vector<const
         UA_CK(cudaMemcpy(hist_host, ws[me].hist.p, sizeof(double) * (hst.iters + 1), cudaMemcpyDeviceToHost));
     res->converged = (hst.bnorm == 0.0) ? 1 : (hst.last_rel <= p.tol);
     res->status = 0;
+    if (sing()) {
+        int herr = 0;
+        for (int r : C.mine) {
+            int h = 0, h2 = 0;
+            UA_CK(cudaMemcpy(&h, ws[r].err.p, sizeof(int), cudaMemcpyDeviceToHost));
+            UA_CK(cudaMemcpy(&h2, ws[r].rws->err.p, sizeof(int), cudaMemcpyDeviceToHost));
+            herr |= h | h2;
+        }
+        if (herr) {
+            res->converged = 0;
+            res->status = UAAMG_ENUMERICAL;
+            throw Error(UAAMG_ENUMERICAL,
+                        "right-hand side at a coarse level has a null-space component (relative size > 1e-10)");
+        }
+    }
     if (hst.status == 1) {
         res->converged = 0;
         res->status = UAAMG_ENUMERICAL;
@@ -764,7 +896,6 @@ int uaamg_dsolve(uaamg_dhier* d, const uaamg_solve_params* p, const double* cons
         std::memset(res, 0, sizeof(*res));
         if (!(p->tol > 0)) throw Error(UAAMG_EINVAL, "tol must be positive");
         DistHier& H = *d->H;
-        if (H.singular) throw Error(UAAMG_EUNSUPPORTED, "sharded solve of a singular (Neumann) hierarchy");
         if (H.Ls() == 0) throw Error(UAAMG_EUNSUPPORTED, "no sharded level (the whole hierarchy is replicated)");
         if (p->inner_krylov_steps > kMaxInner) throw Error(UAAMG_EUNSUPPORTED, "inner_krylov_steps > 16");
         std::lock_guard<std::mutex> lk(d->mu);

@@ -144,8 +144,30 @@ def test_sharded_errors(U, D):
     Dg = U.SparseMatrix(400, 400, np.arange(401), np.arange(400), np.full(400, 2.0))
     with pytest.raises(U.SetupError, match="level 0"):
         D.setup_distributed(Dg, ranks=2, shard_rows=100)
-    # Neumann hierarchies set up sharded, but the sharded solve refuses them
+    # singular (Neumann): a right-hand side with a null-space component
     dh = D.setup_distributed(problems.grid2d(32, "neumann"), ranks=2, shard_rows=100)
     assert dh.singular
-    with pytest.raises(NotImplementedError):
-        D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.zeros(1024))
+    with pytest.raises(U.NumericalError):
+        D.npcg_solve_distributed(dh, U.CycleSpec(), U.Smoother(), np.ones(1024))
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+@pytest.mark.parametrize("kind", ["kcycle", "vcycle"])
+def test_sharded_singular_neumann(U, D, ranks, kind):
+    """Neumann (singular) hierarchy: _check_compatible / _project_mean
+    (U/solvers.py:112-125) folded across ranks; the reference's history
+    within 1e-10, the single-device solve within round-off."""
+    ip, ix, a, g = problem_for("g2d_neu_32")
+    A = _smat(U, ip, ix, a)
+    dh = D.setup_distributed(A, ranks=ranks, shard_rows=100)
+    assert dh.singular and dh.n_sharded >= 2
+    assert_hierarchy_equal(g, _levels(dh))
+    spec = U.CycleSpec(kind=kind)
+    prefix = "" if kind == "kcycle" else "vcycle_"
+    xs, rs = D.npcg_solve_distributed(dh, spec, U.Smoother(), g["b"], tol=float(g["tol"]), max_iters=500)
+    assert_history_close(rs.residual_history, g, prefix=prefix, rtol=1e-10)
+    h = U.setup(A)
+    x1, r1 = U.npcg_solve(h, spec, U.Smoother(), g["b"], tol=float(g["tol"]), max_iters=500)
+    assert rs.iterations == r1.iterations
+    np.testing.assert_allclose(rs.residual_history, r1.residual_history, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(xs, x1, rtol=1e-9, atol=1e-12 * np.abs(x1).max())
