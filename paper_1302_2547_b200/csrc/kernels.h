@@ -22,6 +22,7 @@ struct Groups {
     double* lval = nullptr;      // per long row: its epilogue's reduced values (kMaxLongK each)
     int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per tile
     int tma_rows = 128;          // rows per TMA tile (128, or 64 for dense rows)
+    int tma_rowpar = 0;          // 1: short regular rows, one thread per row (kTmaRowParRows-row tiles)
     __host__ __device__ int units() const { return ng + np; }
 };
 // exact groups (no pieces): every row folded sequentially in reference order

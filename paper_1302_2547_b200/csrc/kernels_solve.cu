@@ -218,6 +218,19 @@ int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base, int rows) {
 
 void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base) {
     static const bool no64 = getenv("UAAMG_NO_TMA64") != nullptr;  // A/B diagnostics
+    static const bool no_rowpar = getenv("UAAMG_NO_ROWPAR") != nullptr;
+    g.tma_rowpar = 0;
+    if (!no_rowpar && max_tile_nnz(n, rp, s, base, 1) <= kTmaRowParMaxRow) {
+        // short rows (7-point-like): thread-per-row tiles beat the gather
+        // (tools/l0_sweep.cu: 0.75 vs 0.69 of HBM at 128^3)
+        const int cap = max_tile_nnz(n, rp, s, base, kTmaRowParRows);
+        if (cap <= kTmaMaxCap) {
+            g.tma_cap = std::max(cap, 4);
+            g.tma_rows = kTmaRowParRows;
+            g.tma_rowpar = 1;
+            return;
+        }
+    }
     int cap = max_tile_nnz(n, rp, s, base, kTmaRows);
     if (cap <= kTmaMaxCap) {
         g.tma_cap = std::max(cap, 4);

@@ -44,8 +44,10 @@ void run_map(int n, const Body& body, Exec ex) {
 template <class Body>
 void run_map(int n, const Body& body, Exec ex);
 
-// TMA-pipelined persistent tiles of R rows (occupancy cached per device)
-template <class Src, class Epi, bool Unit, int R>
+// TMA-pipelined persistent tiles of R rows (occupancy cached per device).
+// RowPar: one thread per row folding straight from the staged tile
+// (k_csr_tma_rows, short regular rows); else the warp-cooperative gather.
+template <class Src, class Epi, bool Unit, int R, bool RowPar = false, int S = kTmaStages>
 inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
     static int occ_dev[kMaxDevices], smem_set_dev[kMaxDevices];
     static size_t occ_smem_dev[kMaxDevices];
@@ -60,15 +62,19 @@ inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi&
     int& occ = occ_dev[dev];
     int& smem_set = smem_set_dev[dev];
     size_t& occ_smem = occ_smem_dev[dev];
-    const size_t smem = tma_smem_bytes(G.tma_cap, R);
-    auto kfn = k_csr_tma<Src, Epi, Unit, R>;
+    constexpr int threads = RowPar ? R : kTmaThreads;
+    const size_t smem = tma_smem_bytes(G.tma_cap, R, S);
+    auto kfn = [] {
+        if constexpr (RowPar) return k_csr_tma_rows<Src, Epi, Unit, R, S>;
+        else return k_csr_tma<Src, Epi, Unit, R, S>;
+    }();
     if ((int)smem > smem_set) {
         UA_CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = (int)smem;
         occ = -1;
     }
     if (occ < 0 || occ_smem != smem) {
-        UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaThreads, smem));
+        UA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem));
         occ_smem = smem;
     }
     const int ntiles = cdiv(G.n, R);
@@ -76,7 +82,7 @@ inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi&
     // matrix streams larger than half the L2 are loaded evict-first
     static const bool no_hint = getenv("UAAMG_NO_L2HINT") != nullptr;  // A/B diagnostics
     const int hint = !no_hint && 12.0 * (double)G.tma_cap * ntiles > kStreamHintBytes;
-    UA_LAUNCH_PDL(kfn, grid, kTmaThreads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi, hint);
+    UA_LAUNCH_PDL(kfn, grid, threads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi, hint);
 }
 
 template <class Src, class Epi, bool Unit>
@@ -89,7 +95,8 @@ inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi&
     if (G.tma_cap > 0 && G.np == 0) {
         // large level: TMA-pipelined persistent tiles (64-row tiles when
         // 128 rows exceed the stage: dense stencils)
-        if (G.tma_rows == 64) launch_tma<Src, Epi, Unit, 64>(A, G, src, epi, ex);
+        if (G.tma_rowpar) launch_tma<Src, Epi, Unit, kTmaRowParRows, true, 2>(A, G, src, epi, ex);
+        else if (G.tma_rows == 64) launch_tma<Src, Epi, Unit, 64>(A, G, src, epi, ex);
         else launch_tma<Src, Epi, Unit, kTmaRows>(A, G, src, epi, ex);
         return;
     }

@@ -117,23 +117,44 @@ int main(int argc, char** argv) {
             k_csr_group<SrcVec, EpiSweep, false><<<grid, 32 * kGrpWarps>>>(A, G, SrcVec{x}, ep);
         }, bytes);
         // max nonzeros per tile (regular stencil: interior bound), 128- and 64-row tiles
-        auto tma = [&](auto rows_tag) {
+        auto tma = [&](auto rows_tag, auto stages_tag) {
             constexpr int R = decltype(rows_tag)::value;
+            constexpr int S = decltype(stages_tag)::value;
             const int cap = st * R;
             if (cap > kTmaMaxCap) return;
-            const size_t smem = tma_smem_bytes(cap, R);
-            auto kfn = k_csr_tma<SrcVec, EpiSweep, false, R>;
+            const size_t smem = tma_smem_bytes(cap, R, S);
+            auto kfn = k_csr_tma<SrcVec, EpiSweep, false, R, S>;
             cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTmaThreads, smem);
             const int ntiles = cdiv(N, R);
             const int grid = std::min(ntiles, kNumSMs * occ);
             char nm[64];
-            snprintf(nm, sizeof nm, "tma%d sweep (%d CTA/SM, %zu B)", R, occ, smem);
+            snprintf(nm, sizeof nm, "tma%d s%d (%d CTA/SM, %zu B)", R, S, occ, smem);
             timeit(nm, [&] { kfn<<<grid, kTmaThreads, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep, 0); }, bytes);
         };
-        tma(std::integral_constant<int, 128>{});
-        tma(std::integral_constant<int, 64>{});
+        tma(std::integral_constant<int, 128>{}, std::integral_constant<int, 3>{});
+        tma(std::integral_constant<int, 64>{}, std::integral_constant<int, 3>{});
+        auto tmar = [&](auto rows_tag, auto stages_tag) {
+            constexpr int R = decltype(rows_tag)::value;
+            constexpr int S = decltype(stages_tag)::value;
+            const int cap = st * R;
+            if (cap > 4096) return;
+            const size_t smem = tma_smem_bytes(cap, R, S);
+            auto kfn = k_csr_tma_rows<SrcVec, EpiSweep, false, R, S>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, R, smem);
+            const int ntiles = cdiv(N, R);
+            const int grid = std::min(ntiles, kNumSMs * occ);
+            char nm[64];
+            snprintf(nm, sizeof nm, "rows%d s%d (%d CTA/SM, %zu B)", R, S, occ, smem);
+            timeit(nm, [&] { kfn<<<grid, R, smem>>>(A, 0, (int)N, ntiles, cap, SrcVec{x}, ep, 0); }, bytes);
+        };
+        tmar(std::integral_constant<int, 128>{}, std::integral_constant<int, 3>{});
+        tmar(std::integral_constant<int, 128>{}, std::integral_constant<int, 2>{});
+        tmar(std::integral_constant<int, 256>{}, std::integral_constant<int, 2>{});
+        tmar(std::integral_constant<int, 64>{}, std::integral_constant<int, 3>{});
         const size_t words = (size_t)(bytes / 2) / 16;
         void *src, *dst;
         cudaMalloc(&src, words * 16 + 64);
