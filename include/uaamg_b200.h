@@ -142,6 +142,16 @@ typedef struct {
  * (message as the reference's SetupError). */
 int uaamg_setup(int n, int64_t nnz, const int *row_ptr, const int *col, const double *val,
                 const uaamg_setup_params *params, uaamg_hierarchy **out, void *stream);
+/* The same setup from the reference's HOST layout (U/sparse.py SparseMatrix:
+ * int64 indptr / indices, float64 data, in host memory) -- the drop-in for a
+ * caller that holds the reference's matrix (U/hierarchy.py:120 called on a
+ * SparseMatrix).  The library uploads the arrays through pinned staging,
+ * narrowing the indices to int32 on the way, and uploads the values WHILE
+ * the level-0 aggregation runs (it reads only the pattern).  Level 0 is
+ * owned by the hierarchy; params->borrow is ignored.  The host arrays may be
+ * reused as soon as the call returns. */
+int uaamg_setup_host(int64_t n, int64_t nnz, const int64_t *indptr, const int64_t *indices, const double *data,
+                     const uaamg_setup_params *params, uaamg_hierarchy **out, void *stream);
 void uaamg_hierarchy_free(uaamg_hierarchy *h);
 
 typedef struct {

@@ -87,6 +87,7 @@ _SIGS = {
     "uaamg_k_smooth_sweeps": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
     "uaamg_aggregate": (_i, [_i, _vp, _vp, _vp, _u64, _i, _i64, _vp, _vp, _vp, _vp]),
     "uaamg_setup": (_i, [_i, _i64, _vp, _vp, _vp, ctypes.POINTER(SetupParams), ctypes.POINTER(_vp), _vp]),
+    "uaamg_setup_host": (_i, [_i64, _i64, _vp, _vp, _vp, ctypes.POINTER(SetupParams), ctypes.POINTER(_vp), _vp]),
     "uaamg_hierarchy_free": (None, [_vp]),
     "uaamg_hierarchy_get_info": (_i, [_vp, ctypes.POINTER(HierarchyInfo)]),
     "uaamg_hierarchy_level": (_i, [_vp, _i, ctypes.POINTER(LevelView)]),

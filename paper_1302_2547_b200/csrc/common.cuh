@@ -245,4 +245,9 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* parti
     }
 }
 
+// pinned-ring host <-> device transfers (hostio.cu): element size se -> de
+// (equal: copy; 8 -> 4: int64 -> int32 narrowing while staging)
+void staged_h2d(void* dst, const void* src, size_t count, int se, int de, cudaStream_t s);
+void staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 }  // namespace uaamg

@@ -154,9 +154,6 @@ std::unique_ptr<DistHier> dist_setup(std::shared_ptr<Comm> C, int n, const int* 
                                      const std::vector<const double*>& av, const std::vector<long long>& nnz,
                                      const uaamg_setup_params& P, long long shard_rows);
 
-uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
-                            const uaamg_setup_params& P, cudaStream_t s, int level_offset);
-
 Part level0_part(int n, int P);
 // renumbering by ascending seed (U/aggregation.py:199-203): rank q's
 // aggregates are [b[q], b[q+1]) with b the exclusive scan of the per-rank

@@ -43,7 +43,9 @@ Ring& ring(int dev) {
 int threads() {
     static const int t = [] {
         const int c = omp_get_num_procs();
-        return c < 2 ? 1 : (c > 8 ? 8 : c);
+        const char* e = getenv("UAAMG_STAGE_THREADS");  // A/B diagnostics
+        const int cap = e ? atoi(e) : 8;
+        return c < 2 ? 1 : (c > cap ? cap : c);
     }();
     return t;
 }

@@ -1464,9 +1464,10 @@ static void exclusive_scan(const T* in, T* out, int n, cudaStream_t s) {
 
 // aggregate() on device.  state arrays are n-sized scratch.
 int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes, long long size_cap,
-                     int* v2a, int* seeds, cudaStream_t s, AggStats* stats) {
+                     int* v2a, int* seeds, cudaStream_t s, AggStats* stats, const std::function<void()>* overlap) {
     const int n = A.n;
     if (n <= 0) throw Error(UAAMG_EAGG, "cannot aggregate an empty matrix");
+    if (overlap && size_cap > 0) (*overlap)();
     const int G = grid_for(n);
     SPtr<uint8_t> st{scratch<uint8_t>(2, n)}, adm{scratch<uint8_t>(3, n)};
     SPtr<double> sc{scratch<double>(4, n)}, ms{scratch<double>(5, n)};
@@ -1556,6 +1557,7 @@ int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes
                                               256, args, 0, s));
         }
         g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (overlap) (*overlap)();
         UA_CK(cudaMemcpyAsync(h_cnt, ctl.p + 9, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         UA_CK(cudaStreamSynchronize(s));
         passes = h_cnt[0];

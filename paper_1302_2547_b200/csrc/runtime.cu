@@ -128,12 +128,14 @@ static void finish_level(Level& L, cudaStream_t s) {
 }
 
 // aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)
-static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t s) {
+// overlap: host work to run while the (first) aggregation kernel executes
+static void aggregate_level(Level& L, const uaamg_setup_params& P, cudaStream_t s,
+                            const std::function<void()>* overlap = nullptr) {
     DBuf<int> deg(L.n, s);
     launch_degrees(L.csr(), deg.p, s);
     L.v2a.alloc(L.n, s);
     DBuf<int> seeds(L.n, s);
-    int nc = device_aggregate(L.csr(), deg.p, P.seed, P.max_passes, P.size_cap, L.v2a.p, seeds.p, s, nullptr);
+    int nc = device_aggregate(L.csr(), deg.p, P.seed, P.max_passes, P.size_cap, L.v2a.p, seeds.p, s, nullptr, overlap);
     if (P.passes_per_level == 2) {
         // aggregate o galerkin o aggregate, composed (U/hierarchy.py:135-138,
         // U/aggregation.py:206-216)
@@ -182,8 +184,27 @@ cudaStream_t library_stream() {
 
 // level_offset: index of this matrix's level in a larger hierarchy (the
 // replicated coarse part of a sharded setup), for error messages
+// second stream per device for uploads that overlap setup kernels
+static cudaStream_t upload_stream() {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    const int dev = cur_dev();
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(dev);
+    if (it != streams.end()) return it->second;
+    cudaStream_t st;
+    UA_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    streams[dev] = st;
+    return st;
+}
+
+// hc != nullptr: level 0 comes from the reference's host layout (int64
+// indptr / indices, float64 data; rp/ci/av are ignored).  The pattern is
+// uploaded (and narrowed) first; the values follow on a second stream WHILE
+// the level-0 aggregation runs -- it reads only the pattern -- and every
+// value reader (singular check, Galerkin) is ordered after them.
 uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
-                            const uaamg_setup_params& P, cudaStream_t s, int level_offset) {
+                            const uaamg_setup_params& P, cudaStream_t s, int level_offset, const HostCsr* hc) {
     if (n <= 0) throw Error(UAAMG_EINVAL, "matrix must be non-empty");
     const int dev_ = cur_dev();
     static bool pool_configured_dev[kMaxDevices] = {};
@@ -246,7 +267,45 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
     // the TMA tile kernel bulk-copies level-0 slices: sources must be
     // 16-byte aligned (borrowed arrays that are not are copied instead)
     auto a16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-    if (P.borrow && a16(rp) && a16(ci) && a16(av)) {
+    std::function<void()> upload_values;
+    bool values_pending = false;
+    struct EvGuard {
+        cudaEvent_t e = nullptr;
+        ~EvGuard() {
+            if (e) cudaEventDestroy(e);
+        }
+    } evg;
+    cudaEvent_t& ev_values = evg.e;
+    if (hc) {
+        L0->rp.alloc(n + 1, s);
+        L0->ci.alloc(std::max(nnz, 1ll), s);
+        L0->av.alloc(std::max(nnz, 1ll), s);
+        const auto t0 = std::chrono::steady_clock::now();
+        staged_h2d(L0->rp.p, hc->rp, (size_t)n + 1, 8, 4, s);
+        staged_h2d(L0->ci.p, hc->ci, (size_t)nnz, 8, 4, s);
+        if (sprof)
+            fprintf(stderr, "setup pattern upload (host) %8.3f ms\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        values_pending = true;
+        UA_CK(cudaEventCreateWithFlags(&ev_values, cudaEventDisableTiming));
+        // the value buffer's allocation (stream-ordered on s) precedes the
+        // copies; recorded now, before the aggregation is queued behind it
+        UA_CK(cudaEventRecord(ev_values, s));
+        Level* l0 = L0.get();  // (L0 is moved into the level list before this runs)
+        upload_values = [&, l0] {
+            if (!values_pending) return;
+            values_pending = false;
+            cudaStream_t s2 = upload_stream();
+            UA_CK(cudaStreamWaitEvent(s2, ev_values, 0));
+            const auto t0 = std::chrono::steady_clock::now();
+            staged_h2d(l0->av.p, hc->av, (size_t)nnz, 8, 8, s2);
+            if (sprof)
+                fprintf(stderr, "setup values upload (host) %8.3f ms\n",
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            UA_CK(cudaEventRecord(ev_values, s2));
+            UA_CK(cudaStreamWaitEvent(s, ev_values, 0));
+        };
+    } else if (P.borrow && a16(rp) && a16(ci) && a16(av)) {
         // level 0 aliases the caller's arrays (U/hierarchy.py: Level 0 holds A)
         L0->rp.adopt_view(const_cast<int*>(rp), n + 1);
         L0->ci.adopt_view(const_cast<int*>(ci), std::max(nnz, 1ll));
@@ -260,17 +319,24 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
         UA_CK(cudaMemcpyAsync(L0->av.p, av, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
     }
     mark("copy");
+    static const bool upload_first = getenv("UAAMG_UPLOAD_FIRST") != nullptr;  // A/B diagnostics
+    if (upload_first && values_pending) upload_values();
     finish_level(*L0, s);
     mark("groups0");
     SingularCheck scheck;
-    if (P.singular < 0) scheck = singular_launch(*L0, s);
-    else h->singular = (P.singular != 0);
+    if (P.singular >= 0) h->singular = (P.singular != 0);
+    else if (!values_pending) scheck = singular_launch(*L0, s);
     mark("singular");
     const int max_levels = P.max_levels;
     std::unique_ptr<Level> cur = std::move(L0);
     while (cur->n > P.n0 && (int)h->levels.size() < max_levels - 1) {
         const std::string lt = "L" + std::to_string(h->levels.size()) + ".";
-        aggregate_level(*cur, P, s);
+        const bool first = values_pending;
+        aggregate_level(*cur, P, s, values_pending ? &upload_values : nullptr);
+        if (first) {
+            if (values_pending) upload_values();
+            if (P.singular < 0) scheck = singular_launch(*cur, s);
+        }
         mark(lt + "aggregate");
         if (cur->nc == cur->n)
             throw Error(UAAMG_ESETUP, "aggregation stagnated at level " +
@@ -290,6 +356,10 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
         mark(lt + "groups");
         h->levels.push_back(std::move(cur));
         cur = std::move(nxt);
+    }
+    if (values_pending) {  // a single-level hierarchy: no aggregation to overlap
+        upload_values();
+        if (P.singular < 0) scheck = singular_launch(*cur, s);
     }
     h->levels.push_back(std::move(cur));
     if (P.singular < 0) h->singular = singular_result(scheck);
@@ -780,6 +850,21 @@ int uaamg_setup(int n, int64_t nnz, const int* row_ptr, const int* col, const do
             throw Error(UAAMG_EAGG, "passes_per_level must be 1 or 2");
         if (params->max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
         *out = setup_impl(n, nnz, row_ptr, col, val, *params, (cudaStream_t)stream, 0);
+    })
+}
+
+int uaamg_setup_host(int64_t n, int64_t nnz, const int64_t* indptr, const int64_t* indices, const double* data,
+                     const uaamg_setup_params* params, uaamg_hierarchy** out, void* stream) {
+    UA_GUARD({
+        if (!params || !out || !indptr || (nnz > 0 && (!indices || !data))) throw Error(UAAMG_EINVAL, "null argument");
+        if (n <= 0 || n >= (int64_t)1 << 31 || nnz < 0 || nnz >= (int64_t)1 << 31)
+            throw Error(UAAMG_EINVAL, "matrix size out of the int32 device range");
+        if (indptr[0] != 0 || indptr[n] != nnz) throw Error(UAAMG_EINVAL, "indptr must run from 0 to nnz");
+        if (params->passes_per_level != 1 && params->passes_per_level != 2)
+            throw Error(UAAMG_EAGG, "passes_per_level must be 1 or 2");
+        if (params->max_passes < 1) throw Error(UAAMG_EAGG, "max_passes must be >= 1");
+        const HostCsr hc{indptr, indices, data};
+        *out = setup_impl((int)n, nnz, nullptr, nullptr, nullptr, *params, (cudaStream_t)stream, 0, &hc);
     })
 }
 

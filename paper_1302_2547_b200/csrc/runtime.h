@@ -346,4 +346,14 @@ cudaStream_t library_stream();
 std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& p, cudaStream_t s, int mat_levels,
                                   bool inner0 = false);
 
+// level 0 in the reference's host layout (U/sparse.py SparseMatrix)
+struct HostCsr {
+    const int64_t* rp;
+    const int64_t* ci;
+    const double* av;
+};
+uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, const double* av,
+                            const uaamg_setup_params& P, cudaStream_t s, int level_offset,
+                            const HostCsr* hc = nullptr);
+
 }  // namespace uaamg

@@ -1,5 +1,7 @@
 // setup.h -- host-side setup drivers (internal).
 #pragma once
+#include <functional>
+
 #include "kernels.h"
 
 namespace uaamg {
@@ -9,8 +11,11 @@ struct AggStats {
     int leftover = 0;
 };
 
+// overlap (optional): host work run while the aggregation kernel executes
+// (after its launch, before the host reads the result); capped aggregation
+// reads |a_ij|, so there it runs first
 int device_aggregate(const Csr& A, const int* deg, uint64_t seed, int max_passes, long long size_cap, int* v2a,
-                     int* seeds, cudaStream_t s, AggStats* stats);
+                     int* seeds, cudaStream_t s, AggStats* stats, const std::function<void()>* overlap = nullptr);
 void build_members(int n, int nc, const int* v2a, int* agg_ptr, int* members, cudaStream_t s);
 long long device_galerkin(const Csr& A, const int* v2a, int nc, const int* agg_ptr, const int* members,
                           DBuf<int>& rp_c, DBuf<int>& ci_c, DBuf<double>& av_c, cudaStream_t s);

@@ -222,15 +222,41 @@ def detect_singular(a):
     return np.max(np.abs(a.spmv(np.ones(a.n_rows)))) <= 1e-10 * scale
 
 
+def _check_setup(rc, reshape_sweeps):
+    if rc == _lib.UAAMG_EINVAL and reshape_sweeps > 0:
+        from .reshaping import _raise_reshape_error
+        _raise_reshape_error(_lib.last_error())
+    _lib.check(rc)
+
+
 def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0, singular=None,
           reshape_pair_cap=16):
     """Build the hierarchy on the GPU (reference hierarchy.py:120-153).
 
-    ``a``: host SparseMatrix (uploaded once) or DeviceCSR (used in place)."""
+    ``a``: host SparseMatrix (uploaded by the library, the values
+    overlapping the level-0 aggregation; a SparseMatrix whose cached device
+    copy exists uses that) or DeviceCSR (used in place)."""
     if a.n_rows != a.n_cols:
         raise SetupError("matrix must be square")
     if reshape_sweeps > 0 and reshape_pair_cap > 16:
         raise NotImplementedError("reshape_pair_cap > 16: the device enumeration handles pairs of at most 16 vertices")
+    P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
+                         max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
+                         n0=int(n0), max_levels=int(max_levels),
+                         singular=-1 if singular is None else int(bool(singular)),
+                         reshape_sweeps=int(reshape_sweeps), reshape_pair_cap=int(reshape_pair_cap), borrow=0)
+    if not isinstance(a, DeviceCSR) and a._device is None:
+        # the reference's host matrix, not yet on the device: the library
+        # uploads it itself, the values overlapping the level-0 aggregation
+        ip = np.ascontiguousarray(a.indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(a.indices, dtype=np.int64)
+        dv = np.ascontiguousarray(a.data, dtype=np.float64)
+        h = ctypes.c_void_p()
+        rc = _lib.load().uaamg_setup_host(a.n_rows, int(ix.shape[0]), ip.ctypes.data, ix.ctypes.data if ix.size else None,
+                                          dv.ctypes.data if dv.size else None, ctypes.byref(P), ctypes.byref(h),
+                                          stream())
+        _check_setup(rc, reshape_sweeps)
+        return Hierarchy(h)
     d = a if isinstance(a, DeviceCSR) else a.device()
     # level 0 aliases the caller's device arrays when the TMA tile kernel may
     # read them in place (int32/int32/float64, contiguous, 16-byte aligned,
@@ -240,17 +266,10 @@ def setup(a, config=AggregationConfig(), n0=100, max_levels=20, reshape_sweeps=0
                        or d.row_ptr.device != cuda_device()):
         d = DeviceCSR.from_arrays(d.n_rows, d.row_ptr, d.col, d.val)
         borrow = True
-    P = _lib.SetupParams(size_cap=0 if config.size_cap is None else int(config.size_cap), seed=int(config.seed),
-                         max_passes=int(config.max_passes), passes_per_level=int(config.passes_per_level),
-                         n0=int(n0), max_levels=int(max_levels),
-                         singular=-1 if singular is None else int(bool(singular)),
-                         reshape_sweeps=int(reshape_sweeps), reshape_pair_cap=int(reshape_pair_cap), borrow=int(borrow))
+    P.borrow = int(borrow)
     h = ctypes.c_void_p()
     rc = _lib.load().uaamg_setup(d.n_rows, d.nnz, ptr(d.row_ptr), ptr(d.col), ptr(d.val), ctypes.byref(P),
                                  ctypes.byref(h), stream())
-    if rc == _lib.UAAMG_EINVAL and reshape_sweeps > 0:
-        from .reshaping import _raise_reshape_error
-        _raise_reshape_error(_lib.last_error())
-    _lib.check(rc)
+    _check_setup(rc, reshape_sweeps)
     # level 0 aliases the device matrix (as the reference's Level 0 holds A)
     return Hierarchy(h, matrix_owner=d)

@@ -122,3 +122,46 @@ def test_setup_copies_unaligned_or_unpadded_level0(U):
     x2, r2 = U.npcg_solve(ref, U.CycleSpec(), U.Smoother(), np.ones(ip.shape[0] - 1), tol=1e-8)
     assert r1.residual_history == r2.residual_history
     assert U.DeviceCSR.from_host(ref.levels[0].matrix).borrowable()
+
+
+def _hier_state(h):
+    out = []
+    for lev in h.levels:
+        m = lev.matrix
+        ag = lev.aggregation
+        out.append((m.indptr.tobytes(), m.indices.tobytes(), m.data.tobytes(),
+                    None if ag is None else (ag.vertex_to_agg.tobytes(), ag.coarse_vertex_of_agg.tobytes())))
+    return out, h.singular
+
+
+@pytest.mark.parametrize("case,cfg", [("c1_grid2d_256", {}), ("g2d_neu_32", {}), ("g3d7_16", {"size_cap": 4}),
+                                      ("g2d_dir_64", {"passes_per_level": 2}), ("wgraph_3000", {})])
+def test_setup_from_host_layout_matches_device_input(U, case, cfg):
+    """setup() on the reference's host SparseMatrix goes through
+    uaamg_setup_host (int64 arrays staged and narrowed by the library, the
+    values uploaded while level 0 aggregates): the same hierarchy bits and
+    the same solve bits as setup() on a device CSR."""
+    ip, ix, a, g = problem_for(case)
+    n = ip.shape[0] - 1
+    A = U.SparseMatrix(n, n, ip, ix, a)
+    assert A._device is None
+    h_host = U.setup(A, U.AggregationConfig(**cfg))
+    assert A._device is None  # the host path does not leave a cached device copy
+    h_dev = U.setup(U.SparseMatrix(n, n, ip, ix, a).device(), U.AggregationConfig(**cfg))
+    assert _hier_state(h_host) == _hier_state(h_dev)
+    b = g["b"] if g["b"].shape[0] else np.ones(n)
+    x1, r1 = U.npcg_solve(h_host, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500)
+    x2, r2 = U.npcg_solve(h_dev, U.CycleSpec(), U.Smoother(), b, tol=float(g["tol"]), max_iters=500)
+    assert r1.residual_history == r2.residual_history and np.array_equal(x1, x2)
+
+
+def test_setup_from_host_layout_single_level_and_errors(U):
+    from paper_1302_2547_b200 import problems
+    A = problems.grid2d(8)  # 64 rows <= n0: one level, no aggregation to overlap
+    h = U.setup(U.SparseMatrix(A.n_rows, A.n_cols, A.indptr, A.indices, A.data))
+    assert h.n_levels == 1 and not h.singular
+    x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), np.ones(64), tol=1e-10)
+    assert rep.converged
+    Dg = U.SparseMatrix(400, 400, np.arange(401), np.arange(400), np.full(400, 2.0))
+    with pytest.raises(U.SetupError, match="level 0"):
+        U.setup(Dg)
