@@ -225,12 +225,14 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* parti
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) partials[k * nb + blockIdx.x] = tot[k];
-        __threadfence();
-        last = atomicAdd(ticket, 1u) == (unsigned)(nb - 1);
+        // one acq_rel ticket: releases this block's partials, and the last
+        // arriver acquires every other block's (no separate fences)
+        unsigned prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ticket) : "memory");
+        last = prev == (unsigned)(nb - 1);
     }
     __syncthreads();
     if (!last) return;
-    __threadfence();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         double s = 0.0;
@@ -240,8 +242,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[K], double* parti
     }
     if (threadIdx.x == 0) {
         fin(tot);
-        __threadfence();
-        *ticket = 0u;
+        *ticket = 0u;  // (re-read only by a later launch)
     }
 }
 
