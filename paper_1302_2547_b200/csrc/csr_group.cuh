@@ -114,12 +114,12 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
         bool last = false;
         if (lane == 0) {
             G.part[slot] = part;
-            __threadfence();
-            last = atomicAdd(G.ticket + lr, 1u) == (unsigned)(np - 1);
+            unsigned prev;  // acq_rel: releases this piece, the last arriver acquires all
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(G.ticket + lr) : "memory");
+            last = prev == (unsigned)(np - 1);
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
-            __threadfence();
             // all partials loaded at once (lane k: pieces k, k+32, ...), then a
             // fixed-shape warp tree: one L2 round trip instead of np
             double acc = 0.0;
