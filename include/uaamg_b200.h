@@ -368,6 +368,12 @@ int uaamg_solve_profile(const uaamg_hierarchy *h, double *seconds3, double *byte
  * (Diagnostics; UAAMG_NO_TAIL=1 in the environment disables the tail.) */
 int uaamg_tail_info(const uaamg_hierarchy *h, int *level, int *cluster);
 
+/* Which row kernel the solve runs on `level` (diagnostics): 0 warp groups
+ * (csr_group.cuh), 1 TMA tiles with warp-cooperative gathers, 2 TMA tiles
+ * with one thread per row (rows of <= 12 entries), 3 the sliced-ELL copy
+ * (csr_ell.cuh: >= 2^20 rows of 13..32 entries; UAAMG_NO_ELL=1 disables). */
+int uaamg_level_kernel(const uaamg_hierarchy *h, int level, int *kind);
+
 /* U/solvers.py:128-157: one cycle on level `level` from a zero guess. */
 int uaamg_cycle(uaamg_hierarchy *h, const uaamg_solve_params *p, int level, const double *b, double *x,
                 void *stream);

@@ -120,6 +120,7 @@ _SIGS = {
     "uaamg_csr_free": (None, [_vp]),
     "uaamg_solve_profile": (_i, [_vp, _vp, _vp, _vp]),
     "uaamg_tail_info": (_i, [_vp, _vp, _vp]),
+    "uaamg_level_kernel": (_i, [_vp, _i, _vp]),
     "uaamg_cycle": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _vp]),
     "uaamg_smooth": (_i, [_vp, ctypes.POINTER(SolveParams), _i, _vp, _vp, _i, _vp, _vp]),
 }

@@ -23,6 +23,9 @@ struct Groups {
     int tma_cap = 0;             // > 0: TMA tile path usable, max nonzeros per tile
     int tma_rows = 128;          // rows per TMA tile (128, or 64 for dense rows)
     int tma_rowpar = 0;          // 1: short regular rows, one thread per row (kTmaRowParRows-row tiles)
+    const long long* ell_off = nullptr;  // sliced-ELL copy (csr_ell.cuh): taken instead of the tiles
+    const int* ell_col = nullptr;
+    const double* ell_val = nullptr;
     __host__ __device__ int units() const { return ng + np; }
 };
 // exact groups (no pieces): every row folded sequentially in reference order
@@ -40,6 +43,9 @@ struct GroupBuf {
     DBuf<unsigned> ticket;
     DBuf<double> part;
     DBuf<double> lval;
+    DBuf<long long> ell_off;
+    DBuf<int> ell_col;
+    DBuf<double> ell_val;
     Groups g;
 };
 // long_min: rows with more entries become pieces (solve path)
@@ -55,6 +61,9 @@ int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0, int rows = 
 // TMA eligibility of rows [base, base + n): sets g.tma_cap / g.tma_rows
 // (128-row tiles, else 64-row tiles) when a tile's nonzeros fit the stage
 void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base = 0);
+// sliced-ELL copy of a large level whose rows are 13..32 entries long (the
+// 27-point stencils): built into gb when the padding stays under 10 %
+bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s);
 
 // fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
 struct BetaReq {

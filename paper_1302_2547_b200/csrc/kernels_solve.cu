@@ -245,6 +245,45 @@ void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base) {
     }
 }
 
+bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s) {
+    const bool no_ell = getenv("UAAMG_NO_ELL") != nullptr;  // A/B diagnostics (read per setup)
+    const int n = A.n;
+    if (no_ell || n < kEllMinRows || gb.g.np != 0 || gb.g.tma_rowpar) return false;
+    const int maxrow = max_tile_nnz(n, A.rp, s, 0, 1);
+    if (maxrow > kEllMaxRow) return false;
+    const int nsl = cdiv(n, 32);
+    DBuf<long long> slab(nsl + 1, s);
+    UA_CK(cudaMemsetAsync(slab.p, 0, sizeof(long long) * (nsl + 1), s));
+    UA_LAUNCH(k_ell_width, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, 0, A.rp, slab.p);
+    gb.ell_off.alloc(nsl + 1, s);
+    size_t tmp = 0;
+    UA_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, slab.p, gb.ell_off.p, nsl + 1, s));
+    DBuf<char> t(tmp, s);
+    UA_CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, slab.p, gb.ell_off.p, nsl + 1, s));
+    long long tot = 0;
+    UA_CK(cudaMemcpyAsync(&tot, gb.ell_off.p + nsl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    UA_CK(cudaStreamSynchronize(s));
+    static size_t total_mem_dev[kMaxDevices] = {};
+    size_t& total_mem = total_mem_dev[cur_dev()];
+    if (!total_mem) {
+        size_t fr = 0;
+        UA_CK(cudaMemGetInfo(&fr, &total_mem));
+    }
+    // (the copy is 12 B per slab entry: at most a quarter of the device)
+    if ((double)tot > kEllMaxPad * (double)A.nnz || (double)tot * 12.0 > 0.25 * (double)total_mem) {
+        gb.ell_off.release();
+        return false;
+    }
+    gb.ell_col.alloc((size_t)tot, s);
+    gb.ell_val.alloc((size_t)tot, s);
+    UA_LAUNCH(k_ell_fill, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, 0, A.rp, A.ci, A.av,
+              gb.ell_off.p, gb.ell_col.p, gb.ell_val.p);
+    gb.g.ell_off = gb.ell_off.p;
+    gb.g.ell_col = gb.ell_col.p;
+    gb.g.ell_val = gb.ell_val.p;
+    return true;
+}
+
 void build_groups(int n, const int* rp, int long_min, GroupBuf& out, cudaStream_t s, int base) {
     out.g = exact_groups(n, base);
     rp += base;  // local view: row i of the range at rp[i]

@@ -3,6 +3,7 @@
 // cross-rank reduction finish of the sharded solve (shard.cu).
 #pragma once
 #include "csr_group.cuh"
+#include "csr_ell.cuh"
 #include "csr_tma.cuh"
 
 namespace uaamg {
@@ -85,12 +86,28 @@ inline void launch_tma(const Csr& A, const Groups& G, const Src& src, const Epi&
     UA_LAUNCH_PDL(kfn, grid, threads, smem, ex.s, A, G.base, G.base + G.n, ntiles, G.tma_cap, src, epi, hint);
 }
 
+// sliced-ELL rows: 4 CTAs of kEllWarps slices per SM (tools/l0_sweep.cu: 0.94
+// of the measured peak for 27-point 256^3 at 4/SM, 0.89 at 8/SM)
+template <class Src, class Epi, bool Unit>
+inline void launch_ell(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
+    Ell E;
+    E.off = G.ell_off;
+    E.col = G.ell_col;
+    E.val = G.ell_val;
+    const int grid = std::max(1, std::min(cdiv(cdiv(G.n, 32), kEllWarps), 4 * kNumSMs));
+    UA_LAUNCH_PDL((k_ell<Src, Epi, Unit>), grid, 32 * kEllWarps, 0, ex.s, A, G.base, G.n, E, src, epi);
+}
+
 template <class Src, class Epi, bool Unit>
 inline void run_stream(const Csr& A, const Groups& G, const Src& src, const Epi& epi, Exec ex) {
     // an empty range still launches when it must publish a (zero) reduction
     if (G.units() == 0) {
         if constexpr (Epi::K == 0) return;
         else if (epi.red.xslot == nullptr) return;
+    }
+    if (G.ell_off) {
+        launch_ell<Src, Epi, Unit>(A, G, src, epi, ex);
+        return;
     }
     if (G.tma_cap > 0 && G.np == 0) {
         // large level: TMA-pipelined persistent tiles (64-row tiles when

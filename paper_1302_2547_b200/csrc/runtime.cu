@@ -120,11 +120,14 @@ static bool singular_result(SingularCheck& c) {
     return ax <= 1e-10 * scale;
 }
 
-static void finish_level(Level& L, cudaStream_t s) {
+// values_ready = false: the level's values are still being uploaded (host
+// layout setup); its ELL copy is built once they are (set_ell)
+static void finish_level(Level& L, cudaStream_t s, bool values_ready = true) {
     build_groups(L.n, L.rp.p, kSolveLongMin, L.grp, s);
     static const bool no_tma = getenv("UAAMG_NO_TMA") != nullptr;  // A/B diagnostics
     static const long long tma_min = getenv("UAAMG_TMA_MIN_ROWS") ? atoll(getenv("UAAMG_TMA_MIN_ROWS")) : kTmaMinRows;
     if (!no_tma && L.n >= tma_min && L.grp.g.np == 0) set_tma(L.grp.g, L.n, L.rp.p, s);
+    if (values_ready) set_ell(L.grp, L.csr(), s);
 }
 
 // aggregation of one level into L.v2a/L.seeds/L.nc (+ passes_per_level=2)
@@ -321,7 +324,7 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
     mark("copy");
     static const bool upload_first = getenv("UAAMG_UPLOAD_FIRST") != nullptr;  // A/B diagnostics
     if (upload_first && values_pending) upload_values();
-    finish_level(*L0, s);
+    finish_level(*L0, s, !values_pending);
     mark("groups0");
     SingularCheck scheck;
     if (P.singular >= 0) h->singular = (P.singular != 0);
@@ -336,6 +339,7 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
         if (first) {
             if (values_pending) upload_values();
             if (P.singular < 0) scheck = singular_launch(*cur, s);
+            set_ell(cur->grp, cur->csr(), s);  // (ordered after the value upload)
         }
         mark(lt + "aggregate");
         if (cur->nc == cur->n)
@@ -360,6 +364,7 @@ uaamg_hierarchy* setup_impl(int n, long long nnz, const int* rp, const int* ci, 
     if (values_pending) {  // a single-level hierarchy: no aggregation to overlap
         upload_values();
         if (P.singular < 0) scheck = singular_launch(*cur, s);
+        set_ell(cur->grp, cur->csr(), s);
     }
     h->levels.push_back(std::move(cur));
     if (P.singular < 0) h->singular = singular_result(scheck);
@@ -951,6 +956,14 @@ int uaamg_solve_profile(const uaamg_hierarchy* h, double* seconds3, double* byte
         bytes3[2] = csr + 40.0 * n;             // direction SpMV: z, p_prev, r in; p, Ap out
         for (int k = 0; k < 3; ++k) seconds3[k] = h->ws->prof_seconds[k];
         *count = h->ws->prof_count;
+    })
+}
+
+int uaamg_level_kernel(const uaamg_hierarchy* h, int level, int* kind) {
+    UA_GUARD({
+        if (!h || !kind || level < 0 || level >= (int)h->levels.size()) throw Error(UAAMG_EINVAL, "bad level");
+        const Groups& g = h->levels[level]->groups();
+        *kind = g.ell_off ? 3 : g.tma_cap > 0 ? (g.tma_rowpar ? 2 : 1) : 0;
     })
 }
 

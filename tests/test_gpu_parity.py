@@ -373,3 +373,36 @@ def test_27pt_tma64_level0_vs_oracle(U, oracle):
     h1, h2 = np.array(rep.residual_history), np.array(ro.residual_history)
     err = np.where(np.abs(h1 - h2) <= 1e-13, 0, np.abs(h1 - h2) / h2)
     assert err.max() <= 1e-10
+
+
+def test_ell_level0_matches_tile_kernels(U, oracle):
+    """27-point level 0 above 2^20 rows takes the sliced-ELL copy
+    (csr_ell.cuh); the solve equals the tile-kernel path (UAAMG_NO_ELL) --
+    same row sums (reference order), so the histories differ only by the
+    dot products' reduction tree.  (Full size: test_gpu_fullsize C4.)"""
+    import ctypes
+    import os
+    from paper_1302_2547_b200 import _lib, problems
+
+    def kind(h, l):
+        k = ctypes.c_int()
+        _lib.check(_lib.load().uaamg_level_kernel(h._handle, l, ctypes.byref(k)))
+        return k.value
+    A = problems.grid3d_device(104, 27)  # 1,124,864 rows
+    out = {}
+    for mode in ("ell", "tiles"):
+        if mode == "tiles":
+            os.environ["UAAMG_NO_ELL"] = "1"
+        try:
+            h = U.setup(A)
+            assert kind(h, 0) == (3 if mode == "ell" else 1)
+            b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+            x, rep = U.npcg_solve(h, U.CycleSpec(), U.Smoother(), b, tol=1e-10, max_iters=300)
+            out[mode] = (x.cpu().numpy(), np.asarray(rep.residual_history), [l.n for l in h.levels])
+        finally:
+            os.environ.pop("UAAMG_NO_ELL", None)
+    assert out["ell"][2] == out["tiles"][2]
+    h1, h2 = out["ell"][1], out["tiles"][1]
+    assert len(h1) == len(h2)
+    assert np.max(np.abs(h1 - h2) / np.abs(h2)) < 1e-12
+    np.testing.assert_allclose(out["ell"][0], out["tiles"][0], rtol=1e-9, atol=1e-12)

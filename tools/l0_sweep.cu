@@ -11,6 +11,8 @@
 
 #include "../paper_1302_2547_b200/csrc/csr_group.cuh"
 #include "../paper_1302_2547_b200/csrc/csr_tma.cuh"
+#include "../paper_1302_2547_b200/csrc/csr_ell.cuh"
+#include <cub/cub.cuh>
 
 using namespace uaamg;
 namespace uaamg {
@@ -135,6 +137,37 @@ int main(int argc, char** argv) {
         };
         tma(std::integral_constant<int, 128>{}, std::integral_constant<int, 3>{});
         tma(std::integral_constant<int, 64>{}, std::integral_constant<int, 3>{});
+        {
+            // sliced ELL copy (csr_ell.cuh)
+            const int nsl = (int)cdiv(N, 32);
+            long long *slab, *off;
+            cudaMalloc(&slab, sizeof(long long) * (nsl + 1));
+            cudaMalloc(&off, sizeof(long long) * (nsl + 1));
+            cudaMemset(slab, 0, sizeof(long long) * (nsl + 1));
+            k_ell_width<<<1184, 256>>>((int)N, 0, rp, slab);
+            size_t tmp = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tmp, slab, off, nsl + 1);
+            void* t;
+            cudaMalloc(&t, tmp);
+            cub::DeviceScan::ExclusiveSum(t, tmp, slab, off, nsl + 1);
+            long long tot = 0;
+            cudaMemcpy(&tot, off + nsl, sizeof(long long), cudaMemcpyDeviceToHost);
+            int* ecol;
+            double* eval;
+            cudaMalloc(&ecol, sizeof(int) * tot);
+            cudaMalloc(&eval, sizeof(double) * tot);
+            k_ell_fill<<<1184, 256>>>((int)N, 0, rp, ci, av, off, ecol, eval);
+            cudaDeviceSynchronize();
+            Ell E;
+            E.off = off; E.col = ecol; E.val = eval;
+            for (int mult : {4, 8, 16}) {
+                const int grid = std::min(cdiv(nsl, kEllWarps), kNumSMs * mult);
+                char nm[64];
+                snprintf(nm, sizeof nm, "ell grid %dxSM (pad %.3f)", mult, (double)tot / nnz);
+                timeit(nm, [&] { k_ell<SrcVec, EpiSweep, false><<<grid, 32 * kEllWarps>>>(A, 0, (int)N, E, SrcVec{x}, ep); }, bytes);
+            }
+            cudaFree(slab); cudaFree(off); cudaFree(t); cudaFree(ecol); cudaFree(eval);
+        }
         auto tmar = [&](auto rows_tag, auto stages_tag) {
             constexpr int R = decltype(rows_tag)::value;
             constexpr int S = decltype(stages_tag)::value;
