@@ -232,6 +232,7 @@ void DistSolve::build() {
             }
             build_groups(Rr.n, Rr.rps, kSolveLongMin, W.gA[l], s, Rr.a);
             if (Rr.n >= kTmaMinRows / 8 && W.gA[l].g.np == 0) set_tma(W.gA[l].g, Rr.n, Rr.rps, s, Rr.a);
+            set_ell(W.gA[l], csr(l, r), s, Rr.n, Rr.a);
             // restriction rows: own aggregates, or all of them into the
             // replicated level
             const int ca = Rr.mbase, cn = Rr.mcount;

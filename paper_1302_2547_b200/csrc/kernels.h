@@ -63,7 +63,8 @@ int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base = 0, int rows = 
 void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base = 0);
 // sliced-ELL copy of a large level whose rows are 13..32 entries long (the
 // 27-point stencils): built into gb when the padding stays under 10 %
-bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s);
+// (rows [base, base + n) of a global-row-indexed CSR; n < 0: all of A)
+bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s, int n = -1, int base = 0);
 
 // fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
 struct BetaReq {

@@ -245,16 +245,16 @@ void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base) {
     }
 }
 
-bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s) {
+bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s, int n, int base) {
     const bool no_ell = getenv("UAAMG_NO_ELL") != nullptr;  // A/B diagnostics (read per setup)
-    const int n = A.n;
+    if (n < 0) n = A.n;
     if (no_ell || n < kEllMinRows || gb.g.np != 0 || gb.g.tma_rowpar) return false;
-    const int maxrow = max_tile_nnz(n, A.rp, s, 0, 1);
+    const int maxrow = max_tile_nnz(n, A.rp, s, base, 1);
     if (maxrow > kEllMaxRow) return false;
     const int nsl = cdiv(n, 32);
     DBuf<long long> slab(nsl + 1, s);
     UA_CK(cudaMemsetAsync(slab.p, 0, sizeof(long long) * (nsl + 1), s));
-    UA_LAUNCH(k_ell_width, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, 0, A.rp, slab.p);
+    UA_LAUNCH(k_ell_width, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, base, A.rp, slab.p);
     gb.ell_off.alloc(nsl + 1, s);
     size_t tmp = 0;
     UA_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, slab.p, gb.ell_off.p, nsl + 1, s));
@@ -270,13 +270,21 @@ bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s) {
         UA_CK(cudaMemGetInfo(&fr, &total_mem));
     }
     // (the copy is 12 B per slab entry: at most a quarter of the device)
-    if ((double)tot > kEllMaxPad * (double)A.nnz || (double)tot * 12.0 > 0.25 * (double)total_mem) {
+    long long nnz = 0;  // this row range's nonzeros
+    {
+        int e[2];
+        UA_CK(cudaMemcpyAsync(&e[0], A.rp + base, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaMemcpyAsync(&e[1], A.rp + base + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UA_CK(cudaStreamSynchronize(s));
+        nnz = (long long)e[1] - e[0];
+    }
+    if ((double)tot > kEllMaxPad * (double)nnz || (double)tot * 12.0 > 0.25 * (double)total_mem) {
         gb.ell_off.release();
         return false;
     }
     gb.ell_col.alloc((size_t)tot, s);
     gb.ell_val.alloc((size_t)tot, s);
-    UA_LAUNCH(k_ell_fill, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, 0, A.rp, A.ci, A.av,
+    UA_LAUNCH(k_ell_fill, std::min(cdiv(nsl * 32, 256), 8 * kNumSMs), 256, 0, s, n, base, A.rp, A.ci, A.av,
               gb.ell_off.p, gb.ell_col.p, gb.ell_val.p);
     gb.g.ell_off = gb.ell_off.p;
     gb.g.ell_col = gb.ell_col.p;
