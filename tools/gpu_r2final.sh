@@ -22,7 +22,7 @@ for st in $STAGES; do
            -k "regex:k_csr_tma_rows" --launch-skip 30 -c 3 -o $OUT/l0_c2 python tools/one_solve.py > $OUT/ncufull.log 2>&1
            echo "ncufull rc=$?" >> $OUT/status.txt ;;
     ncuc4) ONE_SOLVE_N=256 ONE_SOLVE_STENCIL=27 timeout 1200 ncu --set full --clock-control none --import-source on \
-           --kernel-name-base demangled -k "regex:k_csr_tma<.*EpiDirNpcg" -c 1 -o $OUT/l0_c4 python tools/one_solve.py \
+           --kernel-name-base demangled -k "regex:k_ell<.*Epi" -c 3 -o $OUT/l0_c4 python tools/one_solve.py \
            > $OUT/ncuc4.log 2>&1; echo "ncuc4 rc=$?" >> $OUT/status.txt ;;
     configs) timeout 1500 python tools/configs_bench.py C1 C3 C4 C5 > $OUT/configs.jsonl 2> $OUT/configs.err; echo "configs rc=$?" >> $OUT/status.txt ;;
     part) for w in c2slab c4 c5; do timeout 900 python bench.py --workload $w > $OUT/part_$w.json 2> $OUT/part_$w.err; echo "part $w rc=$?" >> $OUT/status.txt; done ;;
