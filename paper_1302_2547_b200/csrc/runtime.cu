@@ -584,7 +584,13 @@ std::unique_ptr<SolveWs> build_ws(uaamg_hierarchy* h, const uaamg_solve_params& 
         in.post = p.post_sweeps;
         in.steps = (!p.kcycle || p.inner_krylov_steps == 0) ? 0 : p.inner_krylov_steps;
         wmark("tail-d2h");
-        if (build_tail(in, ws->tail, s)) ws->tail.Lt = Lt;
+        if (build_tail(in, ws->tail, s)) {
+            ws->tail.Lt = Lt;
+            // the level above: its prolongated iterate comes out of the tail
+            ws->tail.args.xn = U.n;
+            ws->tail.args.xinvm = ws->lev[Lt - 1].invm.p;
+            ws->tail.args.xv2a = U.v2a.p;
+        }
         wmark("tail-build");
     }
     ws->ready = true;

@@ -233,9 +233,17 @@ struct Plan {
         if (tail) {
             double* o = direct ? C.e.p : C.xf.p;
             int* u0 = direct ? nullptr : &ws->fcg.p[l + 1].upd[0];
-            launch_tail(ws->tail, W.r.p, gate, o, u0, s);
+            // the tail also materialises this level's prolongated iterate, so
+            // the post-sweep gathers one array (xmode 1, one post-sweep)
+            const bool xm = xmode == 1 && p.post_sweeps == 1 && ws->tail.args.xn == L.n;
+            launch_tail(ws->tail, W.r.p, gate, o, u0, s, xm ? b : nullptr, xm ? W.tA.p : nullptr);
             ec = o;
             ec_valid = u0;
+            if (xm) {
+                const BetaReq* fb = sing() ? nullptr : br;
+                launch_sweep_vec(A, B, W.invm.p, b, W.tA.p, out, gate, ex(), fb, rs());
+                return fb != nullptr;
+            }
         } else if (direct) {
             cycle(l + 1, C.rhs.p, C.e.p, gate);
             ec = C.e.p;

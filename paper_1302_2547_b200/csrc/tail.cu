@@ -521,6 +521,20 @@ __device__ double tail_cycle(TCtx& c, int vin, int vz, int vapp, int vpp, double
     return -t[0] / t[1];  // BodyBeta::fin
 }
 
+// the level above's prolongated iterate x = 0 + invm b + (valid ? e_c[v2a] : 0)
+// over its rows, split evenly between the CTAs, once every CTA has written
+// its rows of e_c (a.out)
+__device__ void materialise_up(TCtx& c, int valid) {
+    const TailArgs& a = *c.a;
+    csync();
+    const int per = (a.xn + a.cs - 1) / a.cs;
+    const int i1 = min(a.xn, ((int)c.rank + 1) * per);
+    for (int i = (int)c.rank * per + threadIdx.x; i < i1; i += kTailThreads) {
+        const double xp = __dadd_rn(0.0, __dmul_rn(a.xinvm[i], a.xb[i]));
+        a.xout[i] = __dadd_rn(xp, valid ? __ldcg(a.out + a.xv2a[i]) : 0.0);
+    }
+}
+
 __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant__ TailArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const unsigned rank = cta_rank();
@@ -561,6 +575,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant_
         tail_cycle(c, VB, VZ, -1, -1, 0.0, 10);
         const double* z = c.vec(VZ);
         for (int i = threadIdx.x; i < R; i += kTailThreads) a.out[hd.row0 + i] = z[i];
+        if (a.xout) materialise_up(c, 1);
         return;  // last cluster access was before tail_cycle's final barrier
     }
     // ||b||: with a single-aggregate coarsest level it rides in the first
@@ -637,6 +652,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(const __grid_constant_
         for (int i = threadIdx.x; i < R; i += kTailThreads) a.out[hd.row0 + i] = x[i];
     }
     if (rank == 0 && threadIdx.x == 0) *a.upd0 = upd0;
+    if (a.xout) materialise_up(c, upd0);
     TP(60);
     if (a.prof && threadIdx.x < kTailProfMarks) a.prof[rank * kTailProfMarks + threadIdx.x] = g_tp[threadIdx.x];
 }
@@ -917,12 +933,15 @@ void print_tail_prof(const TailPlan& tp) {
     }
 }
 
-void launch_tail(const TailPlan& tp, const double* rprev, const int* gate, double* out, int* upd0, cudaStream_t s) {
+void launch_tail(const TailPlan& tp, const double* rprev, const int* gate, double* out, int* upd0, cudaStream_t s,
+                 const double* xb, double* xout) {
     TailArgs a = tp.args;
     a.rprev = rprev;
     a.gate = gate;
     a.out = out;
     a.upd0 = upd0;
+    a.xb = xb;
+    a.xout = a.xn > 0 ? xout : nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.cs);
     cfg.blockDim = dim3(kTailThreads);

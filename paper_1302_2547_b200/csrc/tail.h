@@ -76,6 +76,14 @@ struct TailArgs {
     double* out = nullptr;          // FCG solution / cycle output of the tail level (global)
     int* upd0 = nullptr;            // FCG step 0 updated x (the prolongation's ec_valid)
     long long* prof = nullptr;      // diagnostics (UAAMG_TAIL_PROF): clock64 per CTA at phase marks
+    // the level above's prolongated iterate, materialised at the end of the
+    // launch (x = 0 + invm b + e_c[v2a], SrcUp's expression) so its post-sweep
+    // gathers one array: static rows / smoother diagonal / map, per-call b, x
+    int xn = 0;
+    const double* xinvm = nullptr;
+    const int* xv2a = nullptr;
+    const double* xb = nullptr;
+    double* xout = nullptr;
 };
 
 // Host inputs for the plan (row-major CSR etc. copied from the device)
@@ -103,6 +111,7 @@ void print_tail_prof(const TailPlan& tp);
 
 // Builds the plan; false if the tail does not fit one cluster's shared memory.
 bool build_tail(const TailInputs& in, TailPlan& tp, cudaStream_t s);
-void launch_tail(const TailPlan& tp, const double* rprev, const int* gate, double* out, int* upd0, cudaStream_t s);
+void launch_tail(const TailPlan& tp, const double* rprev, const int* gate, double* out, int* upd0, cudaStream_t s,
+                 const double* xb = nullptr, double* xout = nullptr);
 
 }  // namespace uaamg
