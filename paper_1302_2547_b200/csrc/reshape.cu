@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kRsThreads) k_reshape_pairs(Csr A, int npairs,
     __shared__ double ah[kRsMax][kRsMax], S[kRsMax][kRsMax], V[kRsMax][kRsMax], E[kRsMax][kRsMax];
     __shared__ double Ap[kRsMax][kRsMax];
     __shared__ double rot[2];
-    __shared__ int m_s, side0;
+    __shared__ int m_s;
     __shared__ double bt[kRsThreads];
     __shared__ long long br[kRsThreads];
     const int b = blockIdx.x;
@@ -99,17 +99,11 @@ __global__ void __launch_bounds__(kRsThreads) k_reshape_pairs(Csr A, int npairs,
         const int m = (pe - p) + (qe - q);
         m_s = m;
         if (m <= cap && m <= kRsMax) {
-            int k = 0;
-            unsigned s1 = 0;
+            int k = 0;  // the union's vertices in ascending order
             while (p < pe || q < qe) {
-                if (q >= qe || (p < pe && members[p] < members[q])) {
-                    s1 |= 1u << k;
-                    mem[k++] = members[p++];
-                } else {
-                    mem[k++] = members[q++];
-                }
+                if (q >= qe || (p < pe && members[p] < members[q])) mem[k++] = members[p++];
+                else mem[k++] = members[q++];
             }
-            side0 = (int)s1;
         }
     }
     __syncthreads();
