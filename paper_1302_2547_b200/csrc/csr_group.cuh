@@ -253,6 +253,13 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
     }
     BodyFcgUpd upd = upd_p;
     upd.alpha = t[1] / t[0];
+    if (upd.last) {  // the last inner step: only x is read afterwards
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+            const double xo = upd.step == 0 ? 0.0 : upd.x[i];
+            upd.x[i] = __dadd_rn(xo, __dmul_rn(upd.alpha, upd.p[i]));
+        }
+        return;
+    }
     double s[1] = {0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) upd.item(i, s);
     grid_reduce_finish<1>(s, upd.red.partials, upd.red.ticket, [&](const double (&tt)[1]) { upd.fin(tt); });

@@ -155,7 +155,7 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
 // levels).  bar: 2 zeroed unsigned, part: >= 2 * kNumSMs * 8 doubles
 void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
-                           RedScratch rs, double* part, unsigned* bar, Exec ex);
+                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last = false);
 // NPCG flavour (have_prev / breakdown handled on device)
 void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);
@@ -173,8 +173,9 @@ void launch_fcg_begin(int n, const double* b, const int* parent_gate, FcgState* 
 void launch_beta(int n, const double* z, const double* pprev, const double* apprev, double* beta, const int* gate,
                  const int* gate2, RedScratch rs, Exec ex);
 // x (+)= alpha p, r_out = r_in - alpha ap, rnorm -> gate[step+1]
+// last: the FCG's last step (only x is read afterwards: no residual / norm)
 void launch_fcg_update(int n, int step, double* x, const double* p, const double* r_in, double* r_out,
-                       const double* ap, FcgState* st, int singular, RedScratch rs, Exec ex);
+                       const double* ap, FcgState* st, int singular, RedScratch rs, Exec ex, bool last = false);
 void launch_npcg_update(int n, double* x, const double* p, double* r, const double* ap, NpcgState* st,
                         double* history, int singular, RedScratch rs, cudaStream_t s);
 // singular helpers: v -= mean(v)   (U/solvers.py:112-113)

@@ -128,11 +128,11 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
 
 void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
-                           RedScratch rs, double* part, unsigned* bar, Exec ex) {
+                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last) {
     static const bool no_fuse = getenv("UAAMG_NO_DIR_FUSE") != nullptr;  // A/B diagnostics
     if (G.tma_cap > 0 || G.n >= kTmaMinRows || no_fuse) {
         launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
-        launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex);
+        launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex, last);
         return;
     }
     EpiDirFcg e{};
@@ -141,6 +141,7 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
     src.z = z; src.pprev = pprev; src.beta_p = &st->beta; src.have_p = nullptr; src.have_static = have_prev;
     BodyFcgUpd u{};
     u.step = step; u.x = x; u.p = p; u.rin = r; u.rout = r_out; u.ap = ap; u.st = st; u.singular = 0;
+    u.last = last ? 1 : 0;
     u.red = {rs.partials, rs.ticket};
     static int maxg_dev[kMaxDevices] = {};
     int& maxg = maxg_dev[cur_dev()];
@@ -461,7 +462,13 @@ void launch_beta(int n, const double* z, const double* pprev, const double* appr
 
 
 void launch_fcg_update(int n, int step, double* x, const double* p, const double* r_in, double* r_out,
-                       const double* ap, FcgState* st, int singular, RedScratch rs, Exec ex) {
+                       const double* ap, FcgState* st, int singular, RedScratch rs, Exec ex, bool last) {
+    if (last && !singular) {
+        BodyFcgUpdLast body{};
+        body.step = step; body.x = x; body.p = p; body.st = st;
+        run_map(n, body, ex);
+        return;
+    }
     BodyFcgUpd body{};
     body.step = step; body.x = x; body.p = p; body.rin = r_in; body.rout = r_out; body.ap = ap; body.st = st;
     body.singular = singular; body.red = {rs.partials, rs.ticket};

@@ -316,7 +316,7 @@ struct Plan {
             if (k > 0 && !fused) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
             if (!sing()) {
                 launch_dir_update_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, x, W.rf.p, st, k, rs(),
-                                      ws->fpart.p, ws->fbar.p + 2 * l, ex());
+                                      ws->fpart.p, ws->fbar.p + 2 * l, ex(), k == p.inner_krylov_steps - 1);
             } else {
                 launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
                 launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());

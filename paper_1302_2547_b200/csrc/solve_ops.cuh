@@ -482,9 +482,29 @@ struct BodyBeta : BodyBase {
 };
 
 // ---- FCG update: x = x + alpha p, r = r - alpha ap, gate[s+1]  (U/solvers.py:181-185,169)
+// the last inner step (step == steps - 1): only x leaves the FCG -- the
+// residual and its norm / gate have no reader, so they are skipped
+struct BodyFcgUpdLast : BodyBase {
+    static constexpr int K = 0;
+    int step;
+    double* x;
+    const double* p;
+    FcgState* st;
+    double alpha;
+    __device__ bool gate() const { return st->upd[step] != 0; }
+    __device__ void off() {}
+    __device__ void init() { alpha = st->alpha; }
+    __device__ void item(int i, double*) {
+        const double xo = step == 0 ? 0.0 : x[i];
+        x[i] = __dadd_rn(xo, __dmul_rn(alpha, p[i]));
+    }
+    __device__ void fin(const double (&)[1]) {}
+};
+
 struct BodyFcgUpd : BodyBase {
     static constexpr int K = 1;
     int step;
+    int last = 0;  // k_dir_update: x only (BodyFcgUpdLast's work)
     double* x;
     const double* p;
     const double* rin;
