@@ -687,7 +687,7 @@ HostRows slice_rows(int r0, int r1, const int* grp, const int* gidx, const doubl
     HostRows h;
     const int R = r1 - r0;
     h.rp.resize(R + 1);
-    const int base = R > 0 ? grp[r0] : 0;
+    const int base = grp[r0];  // (r0 <= n: an empty block starts at row r0 too)
     for (int i = 0; i <= R; ++i) h.rp[i] = grp[r0 + i] - base;
     const int nnz = h.rp[R];
     h.idx.resize(nnz);
