@@ -147,27 +147,30 @@ __device__ __forceinline__ void grp_unit(const Csr& A, const Groups& G, int u, c
     }
 }
 
+// before the dependency wait: pull this warp's first row group of the
+// (read-only) matrix into L1 while the predecessor kernel drains
+template <bool Unit>
+__device__ __forceinline__ void prefetch_first_group(const Csr& A, const Groups& G) {
+    const int u0 = blockIdx.x * kGrpWarps + (threadIdx.x >> 5);
+    if (u0 < G.ng) {
+        const int lane = threadIdx.x & 31;
+        const int r0 = G.base + (u0 << 5);
+        const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + G.base + min((u0 << 5) + 32, G.n));
+        const int cb = (e0 * 4) & ~127, ce = e1 * 4;  // col bytes [cb, ce)
+        for (int o = cb + lane * 128; o < ce; o += 32 * 128) pf(reinterpret_cast<const char*>(A.ci) + o);
+        if (!Unit) {
+            const long long vb = ((long long)e0 * 8) & ~127ll, ve = (long long)e1 * 8;
+            for (long long o = vb + lane * 128; o < ve; o += 32 * 128) pf(reinterpret_cast<const char*>(A.av) + o);
+        }
+    }
+}
+
 // Launch-path kernel: one unit per warp, kGrpWarps warps per CTA, optional
 // deterministic grid reduction (Epi::K > 0) through the ticketed partials.
 template <class Src, class Epi, bool Unit>
 __global__ void __launch_bounds__(32 * kGrpWarps) k_csr_group(Csr A, Groups G, Src src_p, Epi epi_p) {
     __shared__ double win[kGrpWarps][kGrpRound];
-    {
-        // before the dependency wait: pull this warp's first row group of the
-        // (read-only) matrix into L1 while the predecessor kernel drains
-        const int u0 = blockIdx.x * kGrpWarps + (threadIdx.x >> 5);
-        if (u0 < G.ng) {
-            const int lane = threadIdx.x & 31;
-            const int r0 = G.base + (u0 << 5);
-            const int e0 = __ldg(A.rp + r0), e1 = __ldg(A.rp + G.base + min((u0 << 5) + 32, G.n));
-            const int cb = (e0 * 4) & ~127, ce = e1 * 4;  // col bytes [cb, ce)
-            for (int o = cb + lane * 128; o < ce; o += 32 * 128) pf(reinterpret_cast<const char*>(A.ci) + o);
-            if (!Unit) {
-                const long long vb = ((long long)e0 * 8) & ~127ll, ve = (long long)e1 * 8;
-                for (long long o = vb + lane * 128; o < ve; o += 32 * 128) pf(reinterpret_cast<const char*>(A.av) + o);
-            }
-        }
-    }
+    prefetch_first_group<Unit>(A, G);
     pdl_wait();
     pdl_trigger();
     Epi epi = epi_p;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
     __shared__ double win[kGrpWarps][kGrpRound];
     __shared__ double sm[kThreads / 32 + 1];
     __shared__ double tot[2];
+    prefetch_first_group<false>(A, G);
     pdl_wait();
     pdl_trigger();
     EpiDirFcg epi = epi_p;
