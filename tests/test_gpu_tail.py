@@ -44,7 +44,12 @@ def solve_both(U, A, b, spec, sm=None, **kw):
             os.environ["UAAMG_NO_TAIL"] = "1"
         try:
             h = U.setup(A)
-            x, rep = U.npcg_solve(h, spec, sm, b, **kw)
+            try:
+                x, rep = U.npcg_solve(h, spec, sm, b, **kw)
+            except U.NumericalError as e:
+                # a stagnating configuration (no smoothing) may reach an exact
+                # p'Ap = 0 breakdown on either path; compare what ran
+                x, rep = np.zeros(len(b)), e.report
             out[mode] = (np.asarray(x), np.asarray(rep.residual_history), tail_info(h))
         finally:
             os.environ.pop("UAAMG_NO_TAIL", None)
