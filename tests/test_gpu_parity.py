@@ -406,3 +406,40 @@ def test_ell_level0_matches_tile_kernels(U, oracle):
     assert len(h1) == len(h2)
     assert np.max(np.abs(h1 - h2) / np.abs(h2)) < 1e-12
     np.testing.assert_allclose(out["ell"][0], out["tiles"][0], rtol=1e-9, atol=1e-12)
+
+
+def test_ell_cycle_bit_identical_float_weights(U):
+    """Float-weighted 27-point operator above 2^20 rows (random symmetric
+    weights, diagonally dominant): one K-cycle on level 0 through the
+    sliced-ELL copy is BIT-identical to the tile-kernel path -- every row is
+    folded in CSR order without FMA in both, and the cycle's dots live on the
+    coarse levels, which do not change."""
+    import ctypes
+    import os
+    from paper_1302_2547_b200 import _lib, problems
+    A0 = problems.grid3d(104, 27)
+    n = A0.n_rows
+    rows = np.repeat(np.arange(n), np.diff(A0.indptr))
+    cols = A0.indices
+    lo, hi = np.minimum(rows, cols).astype(np.uint64), np.maximum(rows, cols).astype(np.uint64)
+    h64 = (lo * np.uint64(0x9E3779B97F4A7C15) + hi * np.uint64(0xBF58476D1CE4E5B9)) >> np.uint64(11)
+    w = 0.5 + h64.astype(np.float64) / float(1 << 53)  # symmetric, in [0.5, 1.5)
+    data = np.where(rows == cols, 0.0, -w)
+    diag = np.zeros(n)
+    np.add.at(diag, rows, np.abs(data))
+    data = np.where(rows == cols, diag[rows] + 0.25, data)
+    A = U.SparseMatrix(n, n, A0.indptr, A0.indices, data)
+    b = np.sin(np.arange(n) * 0.001) + 1.0
+    out = {}
+    for mode in ("ell", "tiles"):
+        if mode == "tiles":
+            os.environ["UAAMG_NO_ELL"] = "1"
+        try:
+            h = U.setup(A.device())
+            k = ctypes.c_int()
+            _lib.check(_lib.load().uaamg_level_kernel(h._handle, 0, ctypes.byref(k)))
+            assert k.value == (3 if mode == "ell" else 1)
+            out[mode] = U.cycle(h, U.CycleSpec(), U.Smoother(), 0, b)
+        finally:
+            os.environ.pop("UAAMG_NO_ELL", None)
+    assert np.array_equal(out["ell"], out["tiles"])
