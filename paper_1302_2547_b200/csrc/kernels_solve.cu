@@ -219,7 +219,7 @@ int max_tile_nnz(int n, const int* rp, cudaStream_t s, int base, int rows) {
 
 void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base) {
     static const bool no64 = getenv("UAAMG_NO_TMA64") != nullptr;  // A/B diagnostics
-    static const bool no_rowpar = getenv("UAAMG_NO_ROWPAR") != nullptr;
+    const bool no_rowpar = getenv("UAAMG_NO_ROWPAR") != nullptr;  // (read per setup)
     g.tma_rowpar = 0;
     if (!no_rowpar && max_tile_nnz(n, rp, s, base, 1) <= kTmaRowParMaxRow) {
         // short rows (7-point-like): thread-per-row tiles beat the gather

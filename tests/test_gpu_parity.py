@@ -443,3 +443,38 @@ def test_ell_cycle_bit_identical_float_weights(U):
         finally:
             os.environ.pop("UAAMG_NO_ELL", None)
     assert np.array_equal(out["ell"], out["tiles"])
+
+
+def test_rowpar_cycle_bit_identical_float_weights(U):
+    """Float-weighted 7-point operator (rows of <= 7 entries): one K-cycle on
+    level 0 through the row-parallel TMA kernel is BIT-identical to the
+    warp-gather tile kernel (UAAMG_NO_ROWPAR) -- same in-order folds."""
+    import ctypes
+    import os
+    from paper_1302_2547_b200 import _lib, problems
+    A0 = problems.grid3d(96, 7)
+    n = A0.n_rows
+    rows = np.repeat(np.arange(n), np.diff(A0.indptr))
+    cols = A0.indices
+    lo, hi = np.minimum(rows, cols).astype(np.uint64), np.maximum(rows, cols).astype(np.uint64)
+    h64 = (lo * np.uint64(0x9E3779B97F4A7C15) + hi * np.uint64(0xBF58476D1CE4E5B9)) >> np.uint64(11)
+    w = 0.5 + h64.astype(np.float64) / float(1 << 53)
+    data = np.where(rows == cols, 0.0, -w)
+    diag = np.zeros(n)
+    np.add.at(diag, rows, np.abs(data))
+    data = np.where(rows == cols, diag[rows] + 0.25, data)
+    A = U.SparseMatrix(n, n, A0.indptr, A0.indices, data)
+    b = np.cos(np.arange(n) * 0.003) + 1.0
+    out = {}
+    for mode in ("rowpar", "warp"):
+        if mode == "warp":
+            os.environ["UAAMG_NO_ROWPAR"] = "1"
+        try:
+            h = U.setup(A.device())
+            k = ctypes.c_int()
+            _lib.check(_lib.load().uaamg_level_kernel(h._handle, 0, ctypes.byref(k)))
+            assert k.value == (2 if mode == "rowpar" else 1)
+            out[mode] = U.cycle(h, U.CycleSpec(), U.Smoother(), 0, b)
+        finally:
+            os.environ.pop("UAAMG_NO_ROWPAR", None)
+    assert np.array_equal(out["rowpar"], out["warp"])
