@@ -210,6 +210,8 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
     pdl_trigger();
     EpiDirFcg epi = epi_p;
     if (!epi.gate()) {
+        // x keeps the earlier steps' value (valid iff step 0 updated it)
+        if (upd_p.pu.n) upd_p.pu.run(upd_p.x, upd_p.step > 0 && *(volatile const int*)upd_p.pu.valid != 0);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             epi.off();
             upd_p.off();
@@ -252,6 +254,9 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
     const double t[2] = {tot[0], tot[1]};
     if (blockIdx.x == 0 && threadIdx.x == 0) epi.fin(t);  // pap, pr, upd[step], alpha for later readers
     if (!(t[0] > 0.0)) {  // breakdown: the update is gated off (U/solvers.py:179-180)
+        // (step 0 breaking down leaves x invalid; a later step leaves step
+        // 0's x, which then was valid -- this step ran)
+        if (upd_p.pu.n) upd_p.pu.run(upd_p.x, upd_p.step > 0);
         if (blockIdx.x == 0 && threadIdx.x == 0) upd_p.off();
         return;
     }
@@ -261,6 +266,10 @@ __global__ void __launch_bounds__(32 * kGrpWarps) k_dir_update(Csr A, Groups G, 
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
             const double xo = upd.step == 0 ? 0.0 : upd.x[i];
             upd.x[i] = __dadd_rn(xo, __dmul_rn(upd.alpha, upd.p[i]));
+        }
+        if (upd.pu.n) {  // x final everywhere, then the parent's iterate
+            coop_grid_sync(bar);
+            upd.pu.run(upd.x, true);
         }
         return;
     }

@@ -66,6 +66,24 @@ void set_tma(Groups& g, int n, const int* rp, cudaStream_t s, int base = 0);
 // (rows [base, base + n) of a global-row-indexed CSR; n < 0: all of A)
 bool set_ell(GroupBuf& gb, const Csr& A, cudaStream_t s, int n = -1, int base = 0);
 
+// The parent level's prolongated iterate x = 0 + M^-1 b + e_c[v2a] (SrcUp's
+// expression, xmode 1), written by the child FCG's last step once its x
+// (= e_c) is final, so the parent's post-sweep gathers one array.
+struct ParentUp {
+    int n = 0;                 // 0: off
+    const double* invm = nullptr;
+    const double* b = nullptr;
+    const int* v2a = nullptr;
+    const int* valid = nullptr;  // the child FCG's upd[0] (e_c valid)
+    double* out = nullptr;
+    __device__ void run(const double* ec, bool ok) const {
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            const double xp = __dadd_rn(0.0, __dmul_rn(invm[i], b[i]));
+            out[i] = __dadd_rn(xp, ok ? __ldcg(ec + v2a[i]) : 0.0);
+        }
+    }
+};
+
 // fused beta of the flexible CG that consumes a sweep's output (EpiSweepBeta)
 struct BetaReq {
     const double* apprev;
@@ -153,9 +171,12 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
 // fused direction SpMV + update of one flexible-CG step on a small level (one
 // cooperative launch; falls back to the two kernels when recording or on TMA
 // levels).  bar: 2 zeroed unsigned, part: >= 2 * kNumSMs * 8 doubles
-void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
+// pu (last step of a small level's FCG): also materialise the parent level's
+// prolongated iterate; returns whether it did
+bool launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
-                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last = false);
+                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last = false,
+                           const ParentUp* pu = nullptr);
 // NPCG flavour (have_prev / breakdown handled on device)
 void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,
                      double* p, double* ap, NpcgState* st, RedScratch rs, cudaStream_t s);

@@ -126,14 +126,14 @@ void launch_dir_fcg(const Csr& A, const Groups& G, const double* z, const double
     run_stream<SrcDir, EpiDirFcg, false>(A, G, src, e, ex);
 }
 
-void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
+bool launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const double* pprev, int have_prev,
                            const double* r, double* p, double* ap, double* x, double* r_out, FcgState* st, int step,
-                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last) {
+                           RedScratch rs, double* part, unsigned* bar, Exec ex, bool last, const ParentUp* pu) {
     static const bool no_fuse = getenv("UAAMG_NO_DIR_FUSE") != nullptr;  // A/B diagnostics
     if (G.tma_cap > 0 || G.n >= kTmaMinRows || no_fuse) {
         launch_dir_fcg(A, G, z, pprev, have_prev, r, p, ap, st, step, rs, ex);
         launch_fcg_update(A.n, step, x, p, r, r_out, ap, st, 0, rs, ex, last);
-        return;
+        return false;
     }
     EpiDirFcg e{};
     e.p = p; e.ap = ap; e.r = r; e.st = st; e.step = step; e.red = {rs.partials, rs.ticket};
@@ -143,6 +143,7 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
     u.step = step; u.x = x; u.p = p; u.rin = r; u.rout = r_out; u.ap = ap; u.st = st; u.singular = 0;
     u.last = last ? 1 : 0;
     u.red = {rs.partials, rs.ticket};
+    if (last && pu) u.pu = *pu;
     static int maxg_dev[kMaxDevices] = {};
     int& maxg = maxg_dev[cur_dev()];
     if (!maxg) {
@@ -164,6 +165,7 @@ void launch_dir_update_fcg(const Csr& A, const Groups& G, const double* z, const
     cfg.numAttrs = 2;
     UA_CK(cudaLaunchKernelEx(&cfg, k_dir_update<SrcDir>, A, G, src, e, u, part, bar));
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    return u.pu.n > 0;
 }
 
 void launch_dir_npcg(const Csr& A, const Groups& G, const double* z, const double* pprev, const double* r,

@@ -248,7 +248,21 @@ struct Plan {
             cycle(l + 1, C.rhs.p, C.e.p, gate);
             ec = C.e.p;
         } else {
-            fcg(l + 1, C.rhs.p, C.xf.p, gate, begun);
+            // a small child FCG's last step also writes this level's
+            // prolongated iterate (xmode 1), so the post-sweep gathers it
+            ParentUp pu;
+            const bool want = xmode == 1 && p.post_sweeps == 1 && !sing() && L.n < kTmaMinRows &&
+                              !getenv("UAAMG_NO_PARENT_UP");
+            if (want) {
+                pu.n = L.n; pu.invm = W.invm.p; pu.b = b; pu.v2a = L.v2a.p;
+                pu.valid = &ws->fcg.p[l + 1].upd[0]; pu.out = W.tA.p;
+            }
+            const bool xmat = fcg(l + 1, C.rhs.p, C.xf.p, gate, begun, want ? &pu : nullptr);
+            if (xmat) {
+                const BetaReq* fb = sing() ? nullptr : br;
+                launch_sweep_vec(A, B, W.invm.p, b, W.tA.p, out, gate, ex(), fb, rs());
+                return fb != nullptr;
+            }
             ec = C.xf.p;
             ec_valid = &ws->fcg.p[l + 1].upd[0];
         }
@@ -297,7 +311,11 @@ struct Plan {
 
     // U/solvers.py:160-187
     // begun: ||b|| / gate[0] were produced by the caller's restriction
-    void fcg(int l, const double* b, double* x, const int* parent_gate, bool begun = false) {
+    // pu: the parent level's prolongated iterate, written by the last step
+    // when that step is one cooperative kernel (returns whether it was)
+    bool fcg(int l, const double* b, double* x, const int* parent_gate, bool begun = false,
+             const ParentUp* pu = nullptr) {
+        bool xmat = false;
         Level& L = *h->levels[l];
         LevelWs& W = ws->lev[l];
         FcgState* st = ws->fcg.p + l;
@@ -315,13 +333,15 @@ struct Plan {
             const bool fused = cycle(l, rin, W.z.p, g, k > 0 ? &br : nullptr);
             if (k > 0 && !fused) launch_beta(L.n, W.z.p, pp, app, &st->beta, g, nullptr, rs(), ex());
             if (!sing()) {
-                launch_dir_update_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, x, W.rf.p, st, k, rs(),
-                                      ws->fpart.p, ws->fbar.p + 2 * l, ex(), k == p.inner_krylov_steps - 1);
+                const bool last = k == p.inner_krylov_steps - 1;
+                xmat = launch_dir_update_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, x, W.rf.p, st, k,
+                                             rs(), ws->fpart.p, ws->fbar.p + 2 * l, ex(), last, last ? pu : nullptr);
             } else {
                 launch_dir_fcg(L.csr(), L.groups(), W.z.p, pp, k > 0, rin, pc, apc, st, k, rs(), ex());
                 launch_fcg_update(L.n, k, x, pc, rin, W.rf.p, apc, st, sing(), rs(), ex());
             }
         }
+        return xmat;
     }
 
     // one NPCG iteration (U/solvers.py:221-254); parity selects p/p_prev roles

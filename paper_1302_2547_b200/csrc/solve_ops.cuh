@@ -505,6 +505,7 @@ struct BodyFcgUpd : BodyBase {
     static constexpr int K = 1;
     int step;
     int last = 0;  // k_dir_update: x only (BodyFcgUpdLast's work)
+    ParentUp pu;   // (last step only)
     double* x;
     const double* p;
     const double* rin;
